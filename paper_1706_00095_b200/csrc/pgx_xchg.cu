@@ -1,0 +1,732 @@
+// Device-driven per-layer gradient exchange (the fast path).
+//
+// Reference behaviour (pipelined.py:43-218, runtime.py:185-251): as each layer's
+// gradient is emitted by backward, the rank one-sidedly writes it to its
+// reduction parent with a notification; parents fold child contributions in
+// ascending child order, the master applies the update and the new weights flow
+// back down the same tree; no barrier anywhere.  Here the writes are NVLink peer
+// stores issued by this GPU's SMs, notifications are u32 flags raised with a
+// system-scope release, and the waits are device-side acquire spins, so the host
+// never polls.
+//
+//   TREE     the paper's schedule: chunk-pipelined binomial reduce to rank 0,
+//            fused update on rank 0, chunk-pipelined broadcast down the edges.
+//   TWOSHOT  every rank pushes shard j of its gradient into owner j's receive
+//            slot; owner j folds the N contributions in the SAME binomial order
+//            (tree_sum<N>), applies the fused update, and stores the updated
+//            shard straight into every peer's weight buffer.
+//
+// Both give bit-identical weights to the reference fold order.  Work is split
+// into chunks (the notification unit, runtime.py:209-222) claimed through a
+// per-layer atomic queue: every non-waiting push chunk is claimed before any
+// waiting chunk, so a launch makes progress with any number of resident CTAs.
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <vector>
+
+#include "pgx_common.cuh"
+#include "pgx_tree.cuh"
+
+namespace pgx {
+int world_rank(pgx_world* w);
+int world_size(pgx_world* w);
+int world_device(pgx_world* w);
+Status world_status(pgx_world* w);
+bool world_seg(pgx_world* w, int rank, uint32_t id, void** data, uint32_t** flags, uint64_t* size);
+}  // namespace pgx
+
+using namespace pgx;
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr uint64_t kAlignElems = 64;  // 256 B for f32 — layer/shard bases
+
+template <class T>
+struct VecT;
+template <>
+struct VecT<float> {
+  using V = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct VecT<double> {
+  using V = double2;
+  static constexpr int W = 2;
+};
+
+struct Pieces {
+  const void* p[PGX_MAX_PIECES];
+  uint64_t end[PGX_MAX_PIECES];  // cumulative element ends
+  int n;
+};
+
+struct XArgs {
+  Pieces g;                            // this rank's layer gradient
+  void* model[PGX_MAX_RANKS];          // every rank's flat model buffer (element ptr to layer base)
+  uint32_t* mflags[PGX_MAX_RANKS];     // every rank's model-segment flags
+  void* rx[PGX_MAX_RANKS];             // every rank's receive area for this layer
+  uint32_t* rxflags[PGX_MAX_RANKS];    // every rank's rx flags for this layer
+  float* v;                            // momentum (local, layer base)
+  uint32_t* queue;                     // [claim, done]
+  uint64_t S, sl, CH;                  // layer elems, shard elems, chunk elems
+  uint32_t C;                          // chunks per shard (twoshot) / per layer (tree)
+  uint32_t dflag;                      // tree: index of this layer's first down flag in mflags
+  uint32_t layer, epoch;
+  int rank, world, parity, K;          // K: rx slots per parity
+  uint32_t push_items, items;
+  uint32_t item_begin, item_end;       // claimed range (phase selection)
+  double lr;
+  float scale, mu, wd;
+  int mode;
+  Status st;
+};
+
+template <class T>
+__device__ __forceinline__ T grad_elem(const Pieces& P, uint64_t e) {
+  int k = 0;
+  while (k < P.n - 1 && e >= P.end[k]) ++k;
+  uint64_t base = k ? P.end[k - 1] : 0;
+  return static_cast<const T*>(P.p[k])[e - base];
+}
+
+// Load W consecutive gradient elements starting at logical element e (cnt valid).
+template <class T>
+__device__ __forceinline__ void grad_vec(const Pieces& P, uint64_t e, int cnt, T* out) {
+  constexpr int W = VecT<T>::W;
+  int k = 0;
+  while (k < P.n - 1 && e >= P.end[k]) ++k;
+  uint64_t base = k ? P.end[k - 1] : 0;
+  const T* src = static_cast<const T*>(P.p[k]) + (e - base);
+  if (cnt == W && e + W <= P.end[k] && (reinterpret_cast<uintptr_t>(src) % sizeof(typename VecT<T>::V)) == 0) {
+    typename VecT<T>::V v = __ldcs(reinterpret_cast<const typename VecT<T>::V*>(src));
+    memcpy(out, &v, sizeof(v));
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; ++i) out[i] = i < cnt ? grad_elem<T>(P, e + i) : T(0);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void ld_vec(const T* p, int cnt, T* out) {
+  constexpr int W = VecT<T>::W;
+  if (cnt == W) {
+    typename VecT<T>::V v = __ldcg(reinterpret_cast<const typename VecT<T>::V*>(p));
+    memcpy(out, &v, sizeof(v));
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; ++i) out[i] = i < cnt ? __ldcg(p + i) : T(0);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void st_vec(T* p, int cnt, const T* in) {
+  constexpr int W = VecT<T>::W;
+  if (cnt == W) {
+    typename VecT<T>::V v;
+    memcpy(&v, in, sizeof(v));
+    *reinterpret_cast<typename VecT<T>::V*>(p) = v;
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; ++i)
+      if (i < cnt) p[i] = in[i];
+  }
+}
+
+// Fused update of one element (pgx_mode), identical to pgx_ops.cu / the oracle.
+template <class T>
+__device__ __forceinline__ T apply_update(T w, T g, float* v, const XArgs& a) {
+  if constexpr (sizeof(T) == 8) {
+    return __dsub_rn(w, __dmul_rn(a.lr, g));
+  } else {
+    if (a.mode == PGX_MODE_REF32) return __double2float_rn(__dsub_rn((double)w, __dmul_rn(a.lr, (double)g)));
+    float gg = __fadd_rn(__fmul_rn(a.scale, g), __fmul_rn(a.wd, w));
+    float vv = __fadd_rn(__fmul_rn(a.mu, *v), __fmul_rn((float)a.lr, gg));
+    *v = vv;
+    return __fsub_rn(w, vv);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void update_vec(T* w, const T* g, float* v, int cnt, const XArgs& a) {
+  constexpr int W = VecT<T>::W;
+  if constexpr (sizeof(T) == 4) {
+    if (a.mode == PGX_MODE_FAST32) {
+      float vv[W];
+      ld_vec<float>(v, cnt, vv);
+#pragma unroll
+      for (int k = 0; k < W; ++k) w[k] = apply_update<T>(w[k], g[k], &vv[k], a);
+      st_vec<float>(v, cnt, vv);
+      return;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < W; ++k) w[k] = apply_update<T>(w[k], g[k], nullptr, a);
+}
+
+// One thread raises a flag / counter on a peer after the CTA's payload stores.
+__device__ __forceinline__ void cta_release_flag(uint32_t* flag, uint32_t value) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel_sys();
+    st_release_sys(flag, value);
+  }
+}
+
+// Claim the next work item; the last CTA out resets the queue for the next launch.
+__device__ __forceinline__ uint32_t claim(uint32_t* q, uint32_t* smem) {
+  __syncthreads();
+  if (threadIdx.x == 0) *smem = atomicAdd(q, 1u);
+  __syncthreads();
+  return *smem;
+}
+__device__ __forceinline__ void retire(uint32_t* q) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t done = atomicAdd(q + 1, 1u);
+    if (done == gridDim.x - 1) {
+      q[0] = 0;
+      q[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+// Thread i < n waits on flags[i*stride] >= want; then the CTA proceeds.
+__device__ __forceinline__ void cta_wait_flags(uint32_t* const* flags, int n, uint32_t want, const Status& st) {
+  if (threadIdx.x < (unsigned)n) wait_geq(flags[threadIdx.x], want, st);
+  __syncthreads();
+}
+
+// ============================================================== TWOSHOT
+template <int N, class T>
+__global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
+  constexpr int W = VecT<T>::W;
+  __shared__ uint32_t s_item;
+  __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
+  const int me = a.rank;
+  while (true) {
+    uint32_t it = claim(a.queue, &s_item) + a.item_begin;
+    if (it >= a.item_end) break;
+    if (N > 1 && it < a.push_items) {
+      // ---- reduce-scatter push: chunk c of owner j's shard -> j's rx[parity][me]
+      constexpr int NP = N > 1 ? N - 1 : 1;
+      uint32_t c = it / NP;
+      int j = it % NP;
+      j += (j >= me);
+      uint64_t lo = j * a.sl + (uint64_t)c * a.CH;
+      uint64_t hi = min(min(lo + a.CH, (uint64_t)(j + 1) * a.sl), a.S);
+      if (lo < hi) {
+        T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * a.sl + (lo - j * a.sl));
+        uint64_t nvec = (hi - lo + W - 1) / W;
+        for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+          uint64_t e = lo + q * W;
+          int cnt = (int)min((uint64_t)W, hi - e);
+          T buf[W];
+          grad_vec<T>(a.g, e, cnt, buf);
+          st_vec<T>(dst + q * W, cnt, buf);
+        }
+        cta_release_flag(a.rxflags[j] + (uint64_t)me * a.C + c, a.epoch);
+      }
+    } else {
+      // ---- owner: fold N contributions in tree order, update, all-gather store
+      uint32_t c = it - a.push_items;
+      uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
+      uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
+      if (lo >= hi) continue;
+      if (threadIdx.x < N - 1) {
+        int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
+        s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)s * a.C + c;
+      }
+      __syncthreads();
+      cta_wait_flags(s_flags, N - 1, a.epoch, a.st);
+      const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl + (lo - me * a.sl);
+      uint64_t nvec = (hi - lo + W - 1) / W;
+      for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+        uint64_t e = lo + q * W;
+        int cnt = (int)min((uint64_t)W, hi - e);
+        T vals[N][W];
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          if (s == me)
+            grad_vec<T>(a.g, e, cnt, vals[s]);
+          else
+            ld_vec<T>(rxb + (uint64_t)s * a.sl + q * W, cnt, vals[s]);
+        }
+        T* wp = static_cast<T*>(a.model[me]) + e;
+        T w[W];
+        ld_vec<T>(wp, cnt, w);
+        T g[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          T col[N];
+#pragma unroll
+          for (int s = 0; s < N; ++s) col[s] = vals[s][k];
+          if constexpr (sizeof(T) == 8)
+            g[k] = tree_sum<N>(col, AddF64{});
+          else
+            g[k] = tree_sum<N>(col, AddF32{});
+        }
+        update_vec<T>(w, g, a.v ? a.v + e : nullptr, cnt, a);
+        st_vec<T>(wp, cnt, w);
+#pragma unroll
+        for (int s = 0; s < N; ++s)
+          if (s != me) st_vec<T>(static_cast<T*>(a.model[s]) + e, cnt, w);
+      }
+      __syncthreads();
+      if (threadIdx.x < N - 1) {
+        int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
+        fence_acq_rel_sys();
+        red_release_sys_add(a.mflags[s] + a.layer, 1u);
+      }
+    }
+  }
+  retire(a.queue);
+}
+
+// ============================================================== TREE (paper)
+// Up: chunk c: acc = own + child_0 + child_1 + ... (children ascending, each the
+// child's subtree sum), then to the parent's rx slot, or on rank 0 the update
+// and the first hop of the broadcast.
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
+  constexpr int W = VecT<T>::W;
+  __shared__ uint32_t s_item;
+  __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
+  const int me = a.rank;
+  const int nc = tree_num_children(me, a.world);
+  const int parent = tree_parent(me);
+  const int myslot = me ? tree_slot_in_parent(me) : 0;
+  while (true) {
+    uint32_t c = claim(a.queue, &s_item) + a.item_begin;
+    if (c >= a.item_end) break;
+    uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
+    if (threadIdx.x < (unsigned)nc) s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)threadIdx.x * a.C + c;
+    __syncthreads();
+    cta_wait_flags(s_flags, nc, a.epoch, a.st);
+    const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.S;
+    uint64_t nvec = (hi - lo + W - 1) / W;
+    for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+      uint64_t e = lo + q * W;
+      int cnt = (int)min((uint64_t)W, hi - e);
+      T acc[W];
+      grad_vec<T>(a.g, e, cnt, acc);
+      for (int s = 0; s < nc; ++s) {
+        T x[W];
+        ld_vec<T>(rxb + (uint64_t)s * a.S + e, cnt, x);
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          if constexpr (sizeof(T) == 8)
+            acc[k] = __dadd_rn(acc[k], x[k]);
+          else
+            acc[k] = __fadd_rn(acc[k], x[k]);
+        }
+      }
+      if (me == 0) {
+        T* wp = static_cast<T*>(a.model[0]) + e;
+        T w[W];
+        ld_vec<T>(wp, cnt, w);
+        update_vec<T>(w, acc, a.v ? a.v + e : nullptr, cnt, a);
+        st_vec<T>(wp, cnt, w);
+        for (int s = 0; s < nc; ++s) st_vec<T>(static_cast<T*>(a.model[tree_child(0, s)]) + e, cnt, w);
+      } else {
+        T* dst = static_cast<T*>(a.rx[parent]) + ((uint64_t)(a.parity * a.K + myslot) * a.S + e);
+        st_vec<T>(dst, cnt, acc);
+      }
+    }
+    __syncthreads();
+    if (me == 0) {
+      if (threadIdx.x < (unsigned)nc) {
+        int child = tree_child(0, threadIdx.x);
+        fence_acq_rel_sys();
+        st_release_sys(a.mflags[child] + a.dflag + c, a.epoch);
+        red_release_sys_add(a.mflags[child] + a.layer, 1u);
+      }
+    } else if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      st_release_sys(a.rxflags[parent] + (uint64_t)myslot * a.C + c, a.epoch);
+    }
+  }
+  retire(a.queue);
+}
+
+// Down (inner ranks): forward each arrived model chunk to the broadcast children.
+template <class T>
+__global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
+  constexpr int W = VecT<T>::W;
+  __shared__ uint32_t s_item;
+  __shared__ uint32_t* s_flags[1];
+  const int me = a.rank;
+  const int nc = tree_num_children(me, a.world);
+  while (true) {
+    uint32_t c = claim(a.queue, &s_item) + a.item_begin;
+    if (c >= a.item_end) break;
+    uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
+    if (threadIdx.x == 0) s_flags[0] = a.mflags[me] + a.dflag + c;
+    __syncthreads();
+    cta_wait_flags(s_flags, 1, a.epoch, a.st);
+    uint64_t nvec = (hi - lo + W - 1) / W;
+    const T* src = static_cast<const T*>(a.model[me]);
+    for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+      uint64_t e = lo + q * W;
+      int cnt = (int)min((uint64_t)W, hi - e);
+      T w[W];
+      ld_vec<T>(src + e, cnt, w);
+      for (int s = 0; s < nc; ++s) st_vec<T>(static_cast<T*>(a.model[tree_child(me, s)]) + e, cnt, w);
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)nc) {
+      int child = tree_child(me, threadIdx.x);
+      fence_acq_rel_sys();
+      st_release_sys(a.mflags[child] + a.dflag + c, a.epoch);
+      red_release_sys_add(a.mflags[child] + a.layer, 1u);
+    }
+  }
+  retire(a.queue);
+}
+
+// Gate: the stream proceeds once `want` chunk arrivals were counted.
+__global__ void k_gate(const uint32_t* counter, uint32_t want, Status st) {
+  if (threadIdx.x == 0) wait_geq(counter, want, st);
+}
+
+struct LayerPlan {
+  uint64_t S = 0;
+  int variant = 0;
+  uint64_t sl = 0;       // shard elems (twoshot) or S (tree)
+  uint32_t C = 0;        // chunks per shard / per layer
+  int K = 0;             // rx slots per parity
+  uint64_t model_off = 0, rx_off = 0;
+  uint64_t rxflag_off = 0;
+  uint32_t dflag = 0;    // tree down flags index (in mflags)
+  uint32_t push_items = 0, items = 0, down_items = 0;
+  uint32_t expected = 0; // remote chunk arrivals per epoch
+  int grid = 0, down_grid = 0;
+  uint64_t nvlink_bytes = 0, hbm_bytes = 0;
+};
+
+}  // namespace
+
+struct pgx_xchg {
+  pgx_world* w = nullptr;
+  pgx_xchg_config cfg{};
+  int rank = 0, world = 1, dev = 0, esz = 4;
+  std::vector<LayerPlan> L;
+  uint32_t seg_model = 0, seg_rx = 0;
+  void* model = nullptr;
+  uint32_t* mflags = nullptr;
+  void* rx = nullptr;
+  uint32_t* rxflags = nullptr;
+  float* v = nullptr;
+  uint32_t* queues = nullptr;  // 4 per layer
+  void* peer_model[PGX_MAX_RANKS] = {};
+  uint32_t* peer_mflags[PGX_MAX_RANKS] = {};
+  void* peer_rx[PGX_MAX_RANKS] = {};
+  uint32_t* peer_rxflags[PGX_MAX_RANKS] = {};
+  bool connected = false;
+  cudaStream_t down = nullptr;
+  std::vector<cudaEvent_t> done;
+};
+
+namespace {
+
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+int sm_count(int dev) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
+  const LayerPlan& P = x->L[l];
+  XArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int r = 0; r < x->world; ++r) {
+    a.model[r] = static_cast<uint8_t*>(x->peer_model[r]) + P.model_off * x->esz;
+    a.mflags[r] = x->peer_mflags[r];
+    a.rx[r] = static_cast<uint8_t*>(x->peer_rx[r]) + P.rx_off * x->esz;
+    a.rxflags[r] = x->peer_rxflags[r] + P.rxflag_off;
+  }
+  a.v = x->v ? x->v + P.model_off : nullptr;
+  a.S = P.S;
+  a.sl = P.sl;
+  a.CH = x->cfg.chunk_elems;
+  a.C = P.C;
+  a.K = P.K;
+  a.dflag = P.dflag;
+  a.layer = l;
+  a.epoch = iteration + 1;  // notification value = iteration + 1 (runtime.py:205)
+  a.rank = x->rank;
+  a.world = x->world;
+  a.parity = iteration & 1;
+  a.push_items = P.push_items;
+  a.items = P.items;
+  a.lr = x->cfg.lr;
+  a.scale = x->cfg.scale;
+  a.mu = x->cfg.momentum;
+  a.wd = x->cfg.weight_decay;
+  a.mode = x->cfg.mode;
+  a.st = world_status(x->w);
+  return a;
+}
+
+template <class T>
+void launch_twoshot(int N, dim3 g, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n) \
+  case n: k_twoshot<n, T><<<g, kThreads, 0, s>>>(a); break;
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
+  if (!cfg || cfg->num_layers < 1) return fail(PGX_E_CONFIG, "exchange needs at least one layer");
+  if (cfg->chunk_elems < 4 || cfg->chunk_elems % 4) return fail(PGX_E_CONFIG, "chunk_elems must be a positive multiple of 4");
+  if (cfg->mode < 0 || cfg->mode > 2) return fail(PGX_E_CONFIG, "unknown mode %d", cfg->mode);
+  if (!(cfg->lr > 0)) return fail(PGX_E_CONFIG, "epsilon must be > 0, got %g", cfg->lr);
+  pgx_xchg* x = new pgx_xchg();
+  x->w = w;
+  x->cfg = *cfg;
+  x->rank = world_rank(w);
+  x->world = world_size(w);
+  x->dev = world_device(w);
+  x->esz = cfg->mode == PGX_MODE_REF64 ? 8 : 4;
+  x->seg_model = cfg->seg_base;
+  x->seg_rx = cfg->seg_base + 1;
+  const int N = x->world;
+  const uint64_t CH = cfg->chunk_elems;
+  int kmax = 0;
+  for (int r = 0; r < N; ++r) kmax = std::max(kmax, tree_num_children(r, N));
+  int sms = sm_count(x->dev);
+  int cap = cfg->max_ctas > 0 ? cfg->max_ctas : 2 * sms;
+  uint64_t moff = 0, rxoff = 0, rxfoff = 0;
+  uint32_t dflag = cfg->num_layers;
+  x->L.resize(cfg->num_layers);
+  for (int l = 0; l < cfg->num_layers; ++l) {
+    LayerPlan& P = x->L[l];
+    P.S = cfg->layer_elems[l];
+    if (P.S < 1) {
+      delete x;
+      return fail(PGX_E_CONFIG, "layer %d has no elements", l);
+    }
+    P.variant = cfg->variant ? cfg->variant[l] : PGX_VARIANT_TWOSHOT;
+    P.model_off = moff;
+    moff = align_up(moff + P.S, kAlignElems);
+    if (P.variant == PGX_VARIANT_TWOSHOT) {
+      P.sl = align_up((P.S + N - 1) / N, 4);
+      P.C = (uint32_t)((P.sl + CH - 1) / CH);
+      P.K = N;
+      P.rx_off = rxoff;
+      rxoff = align_up(rxoff + 2 * (uint64_t)N * P.sl, kAlignElems);
+      P.rxflag_off = rxfoff;
+      rxfoff += (uint64_t)N * P.C;
+      uint64_t my_lo = std::min(P.S, (uint64_t)x->rank * P.sl), my_hi = std::min(P.S, (uint64_t)(x->rank + 1) * P.sl);
+      uint32_t my_chunks = (uint32_t)((my_hi - my_lo + CH - 1) / CH);
+      P.push_items = (uint32_t)(N - 1) * P.C;
+      P.items = P.push_items + P.C;
+      uint32_t remote = 0;
+      for (int j = 0; j < N; ++j) {
+        if (j == x->rank) continue;
+        uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
+        remote += (uint32_t)((hi - lo + CH - 1) / CH);
+      }
+      P.expected = remote;
+      P.grid = (int)std::min<uint64_t>(P.items, cap);
+      uint64_t own = my_hi - my_lo;
+      P.nvlink_bytes = (N > 1) ? 2ull * (P.S - own) * x->esz : 0;  // RS out + AG out
+      // owner fold: N partial reads + w (+v) read/write; pushes read the rest of the gradient
+      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0)) * own * x->esz +
+                    (P.S - own) * x->esz;
+      (void)my_chunks;
+    } else if (P.variant == PGX_VARIANT_TREE) {
+      P.sl = P.S;
+      P.C = (uint32_t)((P.S + CH - 1) / CH);
+      P.K = std::max(kmax, 1);
+      P.rx_off = rxoff;
+      rxoff = align_up(rxoff + 2 * (uint64_t)P.K * P.S, kAlignElems);
+      P.rxflag_off = rxfoff;
+      rxfoff += (uint64_t)P.K * P.C;
+      P.dflag = dflag;
+      dflag += P.C;
+      P.push_items = 0;
+      P.items = P.C;
+      int nc = tree_num_children(x->rank, N);
+      P.down_items = (x->rank != 0 && nc > 0) ? P.C : 0;
+      P.expected = x->rank == 0 ? 0 : P.C;
+      P.grid = (int)std::min<uint64_t>(P.items, cap);
+      P.down_grid = (int)std::min<uint64_t>(P.down_items, cap);
+      uint64_t out_up = x->rank ? P.S : 0;
+      P.nvlink_bytes = (out_up + (uint64_t)nc * P.S) * x->esz;
+      P.hbm_bytes = ((uint64_t)nc + 1 + (x->rank == 0 ? 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0) : 0)) * P.S * x->esz;
+    } else {
+      delete x;
+      return fail(PGX_E_CONFIG, "layer %d: unknown variant %d", l, P.variant);
+    }
+  }
+  int rc;
+  // model segment: flat weights + [arrival counters | tree down flags]
+  rc = pgx_segment_create(w, x->seg_model, std::max<uint64_t>(moff, 1) * x->esz, dflag, &x->model, &x->mflags);
+  if (rc) { delete x; return rc; }
+  rc = pgx_segment_create(w, x->seg_rx, std::max<uint64_t>(rxoff, 1) * x->esz, (uint32_t)std::max<uint64_t>(rxfoff, 1),
+                          &x->rx, &x->rxflags);
+  if (rc) { delete x; return rc; }
+  {
+    int prev;
+    cudaGetDevice(&prev);
+    cudaSetDevice(x->dev);
+    cudaError_t e = cudaSuccess;
+    if (cfg->mode == PGX_MODE_FAST32) {
+      e = cudaMalloc(&x->v, std::max<uint64_t>(moff, 1) * sizeof(float));
+      if (e == cudaSuccess) e = cudaMemset(x->v, 0, std::max<uint64_t>(moff, 1) * sizeof(float));
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&x->queues, (size_t)cfg->num_layers * 4 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(x->queues, 0, (size_t)cfg->num_layers * 4 * sizeof(uint32_t));
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->down, cudaStreamNonBlocking, hi_prio);
+    x->done.resize(cfg->num_layers);
+    for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l)
+      e = cudaEventCreateWithFlags(&x->done[l], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+      delete x;
+      return fail(PGX_E_CUDA, "exchange allocation failed: %s", cudaGetErrorString(e));
+    }
+  }
+  *out = x;
+  return PGX_OK;
+}
+
+int pgx_xchg_destroy(pgx_xchg* x) {
+  if (!x) return PGX_OK;
+  int prev;
+  cudaGetDevice(&prev);
+  cudaSetDevice(x->dev);
+  cudaDeviceSynchronize();
+  if (x->v) cudaFree(x->v);
+  if (x->queues) cudaFree(x->queues);
+  for (auto e : x->done) cudaEventDestroy(e);
+  if (x->down) cudaStreamDestroy(x->down);
+  cudaSetDevice(prev);
+  delete x;  // segments belong to the world
+  return PGX_OK;
+}
+
+int pgx_xchg_model(pgx_xchg* x, void** model, uint64_t* offsets) {
+  if (model) *model = x->model;
+  if (offsets)
+    for (size_t l = 0; l < x->L.size(); ++l) offsets[l] = x->L[l].model_off;
+  return PGX_OK;
+}
+
+int pgx_xchg_connect(pgx_xchg* x) {
+  for (int r = 0; r < x->world; ++r) {
+    uint64_t sz;
+    if (!world_seg(x->w, r, x->seg_model, &x->peer_model[r], &x->peer_mflags[r], &sz))
+      return fail(PGX_E_ROUTING, "rank %d's model segment %u is not attached", r, x->seg_model);
+    if (!world_seg(x->w, r, x->seg_rx, &x->peer_rx[r], &x->peer_rxflags[r], &sz))
+      return fail(PGX_E_ROUTING, "rank %d's receive segment %u is not attached", r, x->seg_rx);
+  }
+  x->connected = true;
+  return PGX_OK;
+}
+
+int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pieces, const uint64_t* piece_elems,
+                   int npieces, int phases, void* stream) {
+  if (!x->connected) return fail(PGX_E_CONFIG, "exchange not connected");
+  if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
+  if (npieces < 1 || npieces > PGX_MAX_PIECES) return fail(PGX_E_SHAPE, "1..%d gradient pieces, got %d", PGX_MAX_PIECES, npieces);
+  const LayerPlan& P = x->L[l];
+  XArgs a = base_args(x, l, iteration);
+  uint64_t tot = 0;
+  for (int k = 0; k < npieces; ++k) {
+    a.g.p[k] = pieces[k];
+    tot += piece_elems[k];
+    a.g.end[k] = tot;
+  }
+  a.g.n = npieces;
+  if (tot != P.S)
+    return fail(PGX_E_SHAPE, "layer %d gradient has %llu elements, layer needs %llu", l, (unsigned long long)tot,
+                (unsigned long long)P.S);
+  a.queue = x->queues + 4 * l;
+  cudaStream_t s = (cudaStream_t)stream;
+  int prev;
+  cudaGetDevice(&prev);
+  if (prev != x->dev) cudaSetDevice(x->dev);
+  if (P.variant == PGX_VARIANT_TWOSHOT) {
+    a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
+    a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
+    uint32_t n = a.item_end > a.item_begin ? a.item_end - a.item_begin : 0;
+    if (n) {
+      int grid = (int)std::min<uint32_t>(n, (uint32_t)P.grid);
+      if (x->esz == 8)
+        launch_twoshot<double>(x->world, grid, s, a);
+      else
+        launch_twoshot<float>(x->world, grid, s, a);
+    }
+  } else {
+    if (phases & PGX_PHASE_PUSH) {
+      a.item_begin = 0;
+      a.item_end = P.items;
+      if (x->esz == 8)
+        k_tree_up<double><<<P.grid, kThreads, 0, s>>>(a);
+      else
+        k_tree_up<float><<<P.grid, kThreads, 0, s>>>(a);
+    }
+    if (P.down_items && (phases & PGX_PHASE_DOWN)) {
+      XArgs d = a;
+      d.items = P.down_items;
+      d.item_begin = 0;
+      d.item_end = P.down_items;
+      d.queue = a.queue + 2;
+      // the down pass waits on the round trip: its own stream, so later layers'
+      // up passes are not queued behind it (host-stepped callers pass PUSH and
+      // DOWN separately and get the down pass on `stream`)
+      cudaStream_t ds = (phases & PGX_PHASE_PUSH) ? x->down : s;
+      if (x->esz == 8)
+        k_tree_down<double><<<P.down_grid, kThreads, 0, ds>>>(d);
+      else
+        k_tree_down<float><<<P.down_grid, kThreads, 0, ds>>>(d);
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaEventRecord(x->done[l], s);
+  if (prev != x->dev) cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "exchange launch failed: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
+int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
+  if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
+  const LayerPlan& P = x->L[l];
+  cudaStream_t s = (cudaStream_t)stream;
+  int prev;
+  cudaGetDevice(&prev);
+  if (prev != x->dev) cudaSetDevice(x->dev);
+  cudaError_t e = cudaStreamWaitEvent(s, x->done[l], 0);
+  if (e == cudaSuccess && P.expected) {
+    k_gate<<<1, 32, 0, s>>>(x->mflags + l, (iteration + 1) * P.expected, world_status(x->w));
+    e = cudaGetLastError();
+  }
+  if (prev != x->dev) cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "gate failed: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
+int pgx_xchg_layer_bytes(pgx_xchg* x, int l, uint64_t* nvl, uint64_t* hbm) {
+  if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
+  if (nvl) *nvl = x->L[l].nvlink_bytes;
+  if (hbm) *hbm = x->L[l].hbm_bytes;
+  return PGX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+"""DeviceExchange — the device-driven per-layer exchange, wired into PyTorch.
+
+This is the throughput path of the package: the
+reference's per-layer turn (pipelined.py:49-58 publish, :158-188 fold/update,
+:190-203 model arrival) becomes one kernel launch per layer on a high-priority
+communication stream, issued from a post-accumulate-grad hook the moment the
+layer's gradient is final (the `on_layer` contract, net.py:163-172), with all
+waiting done on the device.  The reference's barrier-free `finalize_iteration`
+drain (pipelined.py:60-80) becomes a per-layer *gate* in the next iteration's
+forward-pre-hook: layer l's forward waits only for layer l's new weights.
+
+Weights live in the library's IPC-exported flat model buffer ([W row-major][b]
+per layer, the reference layout net.py:57-63) so peers install updated shards
+directly into them; gradients are read where autograd left them.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+from .errors import ConfigError, ShapeError
+
+VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT}
+MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32}
+
+
+def choose_variant(elems: int, world: int, tree_below: int = 0) -> str:
+    """Layer-size policy: two-shot (reduce-scatter + all-gather) everywhere by default;
+    layers smaller than `tree_below` elements use the paper's tree."""
+    if world > 1 and elems < tree_below:
+        return "tree"
+    return "twoshot"
+
+
+class DeviceExchange:
+    def __init__(self, transport, layer_elems, *, mode: str = "fast32", variant="twoshot",
+                 chunk_elems: int = 16384, lr: float = 0.01, scale: float | None = None,
+                 momentum: float = 0.0, weight_decay: float = 0.0, seg_base: int = 16, max_ctas: int = 0,
+                 tree_below: int = 0):
+        if mode not in MODES:
+            raise ConfigError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
+        self.tr = transport
+        self.world = transport.world_size
+        self.rank = transport.rank
+        self.mode = mode
+        self.layer_elems = [int(n) for n in layer_elems]
+        L = len(self.layer_elems)
+        if isinstance(variant, str) and variant == "auto":
+            variants = [choose_variant(n, self.world, tree_below) for n in self.layer_elems]
+        elif isinstance(variant, str):
+            variants = [variant] * L
+        else:
+            variants = list(variant)
+        if len(variants) != L or any(v not in VARIANTS for v in variants):
+            raise ConfigError(f"bad variant list {variants}")
+        self.variants = variants
+        self.scale = 1.0 / self.world if scale is None else float(scale)
+        self._elems = (C.c_uint64 * L)(*self.layer_elems)
+        self._vars = (C.c_int * L)(*[VARIANTS[v] for v in variants])
+        cfg = _lib.XchgConfig(
+            num_layers=L, layer_elems=self._elems, variant=self._vars, mode=MODES[mode],
+            chunk_elems=int(chunk_elems), lr=float(lr), scale=self.scale, momentum=float(momentum),
+            weight_decay=float(weight_decay), seg_base=int(seg_base), max_ctas=int(max_ctas))
+        h = C.c_void_p()
+        _lib.call("pgx_xchg_create", transport.handle, C.byref(cfg), C.byref(h))
+        self.handle = h
+        self.seg_ids = (seg_base, seg_base + 1)
+        for sid in self.seg_ids:
+            transport.adopt_segment(sid)
+        mp = C.c_void_p()
+        offs = (C.c_uint64 * L)()
+        _lib.call("pgx_xchg_model", h, C.byref(mp), offs)
+        self.model_offsets = [int(o) for o in offs]
+        self.dtype = torch.float64 if mode == "ref64" else torch.float32
+        seg = transport.segment(seg_base)
+        eb = torch.empty((), dtype=self.dtype).element_size()
+        self.model = seg.data[: (seg.size // eb) * eb].view(self.dtype)
+        self.layer_views = [self.model[o:o + n] for o, n in zip(self.model_offsets, self.layer_elems)]
+        with torch.cuda.device(transport.device):
+            self.stream = torch.cuda.Stream(device=transport.device, priority=-1)
+        self.connected = False
+        self.launches = 0
+
+    # -- wiring ----------------------------------------------------------------
+    def connect(self) -> None:
+        """After the transport's rendezvous: resolve every rank's segments."""
+        _lib.call("pgx_xchg_connect", self.handle)
+        self.connected = True
+
+    def layer_bytes(self, layer: int) -> tuple[int, int]:
+        nvl, hbm = C.c_uint64(), C.c_uint64()
+        _lib.call("pgx_xchg_layer_bytes", self.handle, layer, C.byref(nvl), C.byref(hbm))
+        return nvl.value, hbm.value
+
+    # -- per-layer operations ------------------------------------------------------
+    def launch(self, layer: int, iteration: int, pieces, stream=None, phases: int = _lib.PHASE_ALL) -> None:
+        """Exchange layer `layer` of iteration `iteration`; `pieces` are device tensors
+        covering the layer's flat gradient in order (e.g. [dW, db])."""
+        n = len(pieces)
+        if not 1 <= n <= _lib.MAX_PIECES:
+            raise ShapeError(f"1..{_lib.MAX_PIECES} gradient pieces, got {n}")
+        for p in pieces:
+            if p.dtype != self.dtype or not p.is_cuda:
+                raise ShapeError(f"gradient pieces must be {self.dtype} CUDA tensors")
+            if not p.is_contiguous():
+                raise ShapeError("gradient pieces must be contiguous")
+        ptrs = (C.c_void_p * n)(*[p.data_ptr() for p in pieces])
+        cnts = (C.c_uint64 * n)(*[p.numel() for p in pieces])
+        s = (stream or self.stream).cuda_stream
+        _lib.call("pgx_xchg_layer", self.handle, layer, iteration & 0xFFFFFFFF, ptrs, cnts, n, phases, s)
+        self.launches += 1
+
+    def gate(self, layer: int, iteration: int, stream=None) -> None:
+        """Make `stream` (default: current) wait for layer's weights of `iteration`."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.tr.device)
+        _lib.call("pgx_xchg_gate", self.handle, layer, iteration & 0xFFFFFFFF, s.cuda_stream)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None:
+            torch.cuda.synchronize(self.tr.device)
+            _lib.call("pgx_xchg_destroy", self.handle)
+            self.handle = None
+
+
+class ModuleBinding:
+    """Drive a DeviceExchange from an nn.Module's autograd.
+
+    `layers` is a list of (module, [params...]) in model order; layer l's flat
+    vector is the concatenation of its params (W then b, like net.py:57-63).
+    Parameters become views of the exchange's flat model; each layer's exchange
+    launches from the post-accumulate-grad hook of its last-arriving param, on the
+    exchange stream after an event on the compute stream; the module's
+    forward-pre-hook gates on the previous iteration's exchange of that layer.
+    """
+
+    def __init__(self, xchg: DeviceExchange, layers):
+        self.x = xchg
+        self.layers = layers
+        self.k = 0
+        self._pending = [0] * len(layers)
+        self._handles = []
+        for l, (mod, params) in enumerate(layers):
+            n = sum(p.numel() for p in params)
+            if n != xchg.layer_elems[l]:
+                raise ShapeError(f"layer {l} params hold {n} elements, exchange expects {xchg.layer_elems[l]}")
+            view = xchg.layer_views[l]
+            off = 0
+            with torch.no_grad():
+                for p in params:
+                    v = view[off:off + p.numel()].view_as(p)
+                    v.copy_(p.data)
+                    p.data = v
+                    off += p.numel()
+            for p in params:
+                self._handles.append(p.register_post_accumulate_grad_hook(self._make_hook(l)))
+            self._handles.append(mod.register_forward_pre_hook(self._make_gate(l)))
+        self.gpu_launches = 0
+
+    def _make_hook(self, l):
+        def hook(_p):
+            self._pending[l] += 1
+            params = self.layers[l][1]
+            if self._pending[l] < len(params):
+                return
+            self._pending[l] = 0
+            compute = torch.cuda.current_stream(self.x.tr.device)
+            self.x.stream.wait_stream(compute)
+            pieces = []
+            for p in params:
+                g = p.grad
+                if not g.is_contiguous():
+                    g = g.contiguous()
+                g.record_stream(self.x.stream)
+                pieces.append(g)
+            self.x.launch(l, self.k, pieces)
+            for p in params:
+                p.grad = None  # next backward allocates fresh gradients; the allocator
+                # keeps these alive until the exchange stream is past them
+            self.gpu_launches += 1
+        return hook
+
+    def _make_gate(self, l):
+        def pre_hook(_mod, _inp):
+            if self.k > 0:
+                self.x.gate(l, self.k - 1)
+                self.gpu_launches += 1
+        return pre_hook
+
+    def step_done(self) -> None:
+        """Call once per iteration after backward()."""
+        self.k += 1
+
+    def drain(self) -> None:
+        """Gate every layer on the last finished iteration (end of a timed region)."""
+        if self.k > 0:
+            for l in range(len(self.layers)):
+                self.x.gate(l, self.k - 1)
+
+    def remove(self) -> None:
+        for h in self._handles:
+            h.remove()

@@ -1,0 +1,57 @@
+"""The C ABI: libpgx.so loads without a GPU and exports every symbol include/pgx.h declares."""
+
+import ctypes
+import os
+import subprocess
+
+import pytest
+
+from paper_1706_00095_b200 import _lib
+
+
+def test_library_is_built():
+    assert os.path.exists(_lib.LIB_PATH), "run __graft_entry__.build()"
+
+
+def test_every_header_symbol_is_exported_and_bound():
+    declared = _lib.header_symbols()
+    assert len(declared) >= 30
+    handle = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(handle, name), f"{name} declared in pgx.h but not exported"
+    assert set(declared) == set(_lib.SIGNATURES), "ctypes signature table drifted from pgx.h"
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert set(declared) <= exported
+
+
+def test_abi_version_and_error_channel():
+    lib = _lib.lib()
+    assert lib.pgx_abi_version() == 1
+    assert isinstance(_lib.last_error(), str)
+
+
+def test_built_for_sm100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_device_means_a_loud_error_not_a_fallback():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    h = ctypes.c_void_p()
+    rc = _lib.lib().pgx_world_create(0, 1, 0, ctypes.byref(h))
+    assert rc != 0
+    with pytest.raises(Exception):
+        _lib.call("pgx_world_create", 0, 1, 0, ctypes.byref(h))
+
+
+def test_product_path_never_imports_the_oracle():
+    root = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1706_00095_b200")
+    for dirpath, _, files in os.walk(root):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "from oracle" not in src and "import oracle" not in src

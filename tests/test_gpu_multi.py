@@ -1,0 +1,135 @@
+"""Real multi-GPU runs: one process per GPU, CUDA-IPC peer segments, concurrent
+device-side waits over NVLink.  Skipped unless >= 2 GPUs are visible."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+LENET = [520, 25050, 400500, 5010]
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _exchange_worker(rank, world, port, variant, mode, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    from oracle import pipesgd_oracle as O
+    from paper_1706_00095_b200.exchange import DeviceExchange
+    from paper_1706_00095_b200.transport import DistTransport
+
+    try:
+        tr = DistTransport(rank, world, rank, timeout_s=20.0)
+        elems = LENET + [1 << 20]
+        hyper = dict(lr=0.01, momentum=0.9, weight_decay=5e-4) if mode == "fast32" else dict(lr=0.05)
+        x = DeviceExchange(tr, elems, mode=mode, variant=variant, chunk_elems=16384, **hyper)
+        dt = np.float32
+        w = [O.seeded_fill(42 ^ l, n, 1.0 / np.sqrt(n)).astype(dt) for l, n in enumerate(elems)]
+        v = [np.zeros(n, np.float32) for n in elems]
+        for l in range(len(elems)):
+            x.layer_views[l].copy_(torch.from_numpy(w[l]))
+        torch.cuda.synchronize()
+        tr.barrier()  # rendezvous: IPC handles exchanged, peers attached
+        x.connect()
+        comp = torch.cuda.current_stream()
+        bad = []
+        for k in range(4):
+            for l in range(len(elems)):
+                x.gate(l, k - 1) if k else None
+            grads = {}
+            for l in reversed(range(len(elems))):
+                n = elems[l]
+                gs = [O.seeded_fill(O.derived_seed(42, r, l, k), n, 1e-2).astype(dt) for r in range(world)]
+                grads[l] = gs
+                g = torch.from_numpy(gs[rank]).cuda()
+                x.stream.wait_stream(comp)
+                g.record_stream(x.stream)
+                x.launch(l, k, [g])
+            for l in range(len(elems)):
+                if mode == "fast32":
+                    w[l], v[l] = O.exchange_iteration(grads[l], w[l], 0.01, mode, state=v[l], scale=1.0 / world,
+                                                      momentum=0.9, weight_decay=5e-4)
+                else:
+                    w[l] = O.exchange_iteration(grads[l], w[l], 0.05, mode).astype(dt)
+            for l in range(len(elems)):
+                x.gate(l, k)
+            torch.cuda.synchronize()
+            for l in range(len(elems)):
+                if x.layer_views[l].cpu().numpy().tobytes() != w[l].tobytes():
+                    bad.append((k, l))
+        q.put((rank, bad, tr.device_status()))
+        x.close()
+        tr.close()
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, repr(exc), -1))
+    dist.destroy_process_group()
+
+
+def _spawn(fn, world, *args):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=fn, args=(r, world, port, *args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    return sorted(out, key=lambda t: t[0])
+
+
+def _ngpu():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("variant", ["twoshot", "tree"])
+@pytest.mark.parametrize("mode", ["ref32", "fast32"])
+def test_concurrent_exchange_matches_oracle(variant, mode):
+    out = _spawn(_exchange_worker, _ngpu(), variant, mode)
+    for rank, bad, status in out:
+        assert bad == [] and status == 0, (rank, bad, status)
+
+
+def _engine_worker(rank, world, port, pattern, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    from paper_1706_00095_b200 import harness
+    from paper_1706_00095_b200.config import TrainConfig
+
+    try:
+        cfg = TrainConfig(layer_dims=(6, 9, 5), world_size=world, iterations=4, batch_size=24, dataset_size=48,
+                          seed=19, epsilon=0.08, pattern=pattern, finalize_timeout_s=20.0)
+        ds = harness.build_dataset(cfg, device=f"cuda:{rank}")
+        res = harness.run_dist(cfg, ds, rank, rank)
+        ref = harness.sequential_sgd(cfg, ds, device=f"cuda:{rank}")
+        ok = all(a.tobytes() == b.tobytes() for a, b in zip(res.model, ref))
+        q.put((rank, ok, res.barrier_calls))
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, repr(exc), -1))
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("pattern", ["pipelined", "barrier"])
+def test_host_engine_over_ipc_matches_sequential(pattern):
+    out = _spawn(_engine_worker, _ngpu(), pattern)
+    for rank, ok, barriers in out:
+        assert ok is True, (rank, ok)
+        assert barriers == (0 if pattern == "pipelined" else 8)
