@@ -1,0 +1,398 @@
+"""Benchmark: AlexNet (B=256 global, synthetic 227x227) data-parallel SGD with the
+per-layer device exchange — images/sec at N GPUs (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W]                 # our arm
+    python bench.py --impl reference [--gpus N ...]                  # CPU reference arm
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+A step = one training iteration: forward + backward of AlexNet on this rank's
+256/N images (PyTorch/cuDNN, bf16 autocast, fp32 master weights), during which
+every layer's gradient is exchanged and the fused momentum-SGD update applied by
+libpgx kernels as soon as that layer's gradient is final; the next forward of a
+layer waits only for that layer's new weights.  One JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GLOBAL_BATCH = 256
+ALEXNET_LAYERS = [34944, 307456, 885120, 663936, 442624, 37752832, 16781312, 4097000]
+METRIC = "AlexNet images/sec (B=256 global, synthetic 227x227), per-layer gradient exchange"
+NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
+    p.add_argument("--variant", default="twoshot", choices=["twoshot", "tree", "auto"])
+    p.add_argument("--chunk-elems", type=int, default=16384)
+    p.add_argument("--max-ctas", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--timeline", default="")
+    return p.parse_args()
+
+
+def cpu_info():
+    try:
+        model = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")][0]
+    except Exception:  # noqa: BLE001
+        model = "unknown"
+    return model, len(os.sched_getaffinity(0))
+
+
+# ------------------------------------------------------------------ CPU port
+CPU_SAMPLE_IMAGES = 8
+
+
+def _cpu_fwd_bwd(model, x, y):
+    import torch
+
+    loss = torch.nn.functional.cross_entropy(model(x), y)
+    loss.backward()
+    model.zero_grad(set_to_none=True)
+
+
+def cpu_step_timing(world: int, *, steps: int | None = None, seconds: float | None = None, warmup: int = 1):
+    """The same training step on the host CPU: AlexNet forward+backward in PyTorch-CPU
+    fp32 on a bounded sample of CPU_SAMPLE_IMAGES images (per-image cost scaled to the
+    256-image global batch), plus the reference's exchange data plane (tree fold, master
+    update, tree broadcast over `world` ranks) restated in C (oracle/pgx_oracle.c) on the
+    full AlexNet parameter set.  All host threads."""
+    import torch
+
+    from oracle import c_oracle as CO
+
+    model_name, ncpu = cpu_info()
+    torch.set_num_threads(ncpu)
+    net = alexnet()
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(CPU_SAMPLE_IMAGES, 3, 227, 227, generator=g)
+    y = torch.randint(0, 1000, (CPU_SAMPLE_IMAGES,), generator=g)
+    ex = CO.ExchangeWorld(world, ALEXNET_LAYERS)
+    for _ in range(warmup):
+        _cpu_fwd_bwd(net, x, y)
+        ex.iteration("fast32", threads=ncpu)
+    fb, xc = [], []
+    t_end = time.perf_counter() + (seconds or 1e9)
+    while (steps is None or len(fb) < steps) and time.perf_counter() < t_end:
+        t0 = time.perf_counter()
+        _cpu_fwd_bwd(net, x, y)
+        t1 = time.perf_counter()
+        ex.iteration("fast32", lr=0.01, mu=0.9, wd=5e-4, threads=ncpu)
+        t2 = time.perf_counter()
+        fb.append((t1 - t0) * GLOBAL_BATCH / CPU_SAMPLE_IMAGES)
+        xc.append(t2 - t1)
+    t_fb, t_x = statistics.median(fb), statistics.median(xc)
+    t = t_fb + t_x
+    return {"value": GLOBAL_BATCH / t, "unit": "images/s", "cores": ncpu, "kind": "port",
+            "sample": f"{len(fb)} steps; each: AlexNet fwd+bwd of {CPU_SAMPLE_IMAGES} images in PyTorch-CPU fp32 "
+                      f"scaled x{GLOBAL_BATCH // CPU_SAMPLE_IMAGES} to the 256-image batch, plus one full "
+                      f"exchange of the 60,965,224 fp32 params at world {world} (C port of the reference's tree "
+                      f"fold + update + broadcast); cpu {model_name}",
+            "ms_per_step": t * 1e3, "ms_fwd_bwd": t_fb * 1e3, "ms_exchange": t_x * 1e3,
+            "exchange_only_images_per_s": GLOBAL_BATCH / t_x}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return
+    r = cpu_step_timing(world, steps=args.steps, warmup=max(1, min(args.warmup, 2)))
+    line = {"metric": METRIC, "value": r["value"], "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": workload_config(world, args),
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "ms_fwd_bwd",
+                                               "ms_exchange", "exchange_only_images_per_s")},
+            "e2e": {"value": r["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(world, args):
+    return {"workload": "alexnet_b256_synthetic_227", "model": "AlexNet (BVLC, grouped conv, LRN)",
+            "global_batch": GLOBAL_BATCH, "per_gpu_batch": GLOBAL_BATCH // world, "image": [3, 227, 227],
+            "parallelism": f"dp{world}", "exchange": args.variant, "update": "fast32 momentum SGD lr 0.01 mu 0.9 "
+            "wd 5e-4 scale 1/N", "fwd_bwd": "PyTorch cuDNN bf16 autocast, fp32 master weights/grads",
+            "l2": "working set > L2 (244 MB fp32 weights + 244 MB grads + activations per step)",
+            "chunk_elems": args.chunk_elems}
+
+
+# ------------------------------------------------------------------ model
+def alexnet():
+    import torch.nn as nn
+
+    class AlexNet(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.conv1 = nn.Conv2d(3, 96, 11, stride=4)
+            self.conv2 = nn.Conv2d(96, 256, 5, padding=2, groups=2)
+            self.conv3 = nn.Conv2d(256, 384, 3, padding=1)
+            self.conv4 = nn.Conv2d(384, 384, 3, padding=1, groups=2)
+            self.conv5 = nn.Conv2d(384, 256, 3, padding=1, groups=2)
+            self.fc6 = nn.Linear(9216, 4096)
+            self.fc7 = nn.Linear(4096, 4096)
+            self.fc8 = nn.Linear(4096, 1000)
+            self.relu = nn.ReLU(inplace=True)
+            self.lrn = nn.LocalResponseNorm(5, alpha=1e-4, beta=0.75)
+            self.pool = nn.MaxPool2d(3, 2)
+            self.drop = nn.Dropout(0.5)
+
+        def forward(self, x):
+            x = self.pool(self.lrn(self.relu(self.conv1(x))))
+            x = self.pool(self.lrn(self.relu(self.conv2(x))))
+            x = self.relu(self.conv3(x))
+            x = self.relu(self.conv4(x))
+            x = self.pool(self.relu(self.conv5(x)))
+            x = x.flatten(1)
+            x = self.drop(self.relu(self.fc6(x)))
+            x = self.drop(self.relu(self.fc7(x)))
+            return self.fc8(x)
+
+        def layers(self):
+            return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.conv3, self.conv4, self.conv5,
+                                                     self.fc6, self.fc7, self.fc8)]
+
+    return AlexNet()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ our arm
+def pgx_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
+    from paper_1706_00095_b200.transport import DistTransport
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)  # plumbing: handles + timing max
+    torch.backends.cudnn.benchmark = True
+    torch.manual_seed(1234 + rank)
+
+    model = alexnet().to(dev)
+    tr = DistTransport(rank, world, local, timeout_s=60.0)
+    xchg = DeviceExchange(tr, ALEXNET_LAYERS, mode="fast32", variant=args.variant, chunk_elems=args.chunk_elems,
+                          lr=0.01, momentum=0.9, weight_decay=5e-4, scale=1.0 / world, max_ctas=args.max_ctas)
+    bind = ModuleBinding(xchg, model.layers())
+    if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)
+        flat = xchg.model.cpu()
+        dist.broadcast(flat, 0)
+        xchg.model.copy_(flat.to(dev))
+        torch.cuda.synchronize()
+    tr.barrier()      # rendezvous: every rank's segments attached over CUDA IPC
+    xchg.connect()
+
+    B = GLOBAL_BATCH // world
+    g = torch.Generator().manual_seed(42 + rank)
+    host_x = torch.randint(0, 256, (B, 3, 227, 227), dtype=torch.uint8, generator=g).pin_memory()
+    host_y = torch.randint(0, 1000, (B,), dtype=torch.int64, generator=g).pin_memory()
+    dev_x, dev_y = host_x.to(dev), host_y.to(dev)
+    loss_host = torch.zeros(max(args.steps, 1), dtype=torch.float32).pin_memory()
+    crit = torch.nn.CrossEntropyLoss()
+
+    def step(xb, yb):
+        xin = xb.to(torch.bfloat16, memory_format=torch.channels_last).sub_(128.0).mul_(1.0 / 64.0)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            out = model(xin)
+        loss = crit(out.float(), yb)
+        loss.backward()
+        bind.step_done()
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(fn, k):
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(k):
+            fn(i)
+        bind.drain()  # the last iteration's weights are installed everywhere
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for _ in range(args.warmup):
+        step(dev_x, dev_y)
+    bind.drain()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region (value) ----
+    L_DOM = 5  # fc6: the dominant exchange/update kernel (37.75M params)
+    bind.timed_layers = {L_DOM}
+    bind.events.clear()
+    clocks = ClockSampler(local)
+    clocks.start()
+    n0 = xchg.launch_count()
+    ms = timed(lambda i: step(dev_x, dev_y), args.steps)
+    launches = xchg.launch_count() - n0
+    clk = clocks.stop()
+    durs = [a.elapsed_time(b) for a, b in bind.events.get(L_DOM, [])]
+    bind.timed_layers = set()
+    value = GLOBAL_BATCH * args.steps / (ms / 1e3)
+
+    # ---- dominant kernel in isolation (same launch, no concurrent backward) ----
+    gfc6 = [torch.randn(4096, 9216, device=dev) * 1e-3, torch.randn(4096, device=dev) * 1e-3]
+    iso = []
+    if world == 1:
+        for i in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(xchg.stream)
+            xchg.launch(L_DOM, bind.k + i, gfc6)
+            e1.record(xchg.stream)
+            torch.cuda.synchronize()
+            iso.append(e0.elapsed_time(e1))
+        bind.k += 10  # keep the epoch sequence monotone (N=1 has no peer flags)
+
+    # ---- end-to-end through the public API: host batch in, loss out ----
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step(i):
+            xb = host_x.to(dev, non_blocking=True)
+            yb = host_y.to(dev, non_blocking=True)
+            loss = step(xb, yb)
+            loss_host[i % loss_host.numel()].copy_(loss.detach(), non_blocking=True)
+        ms_e2e = timed(e2e_step, args.steps)
+        h2d = (host_x.numel() * host_x.element_size() + host_y.numel() * host_y.element_size()) * world
+        e2e = {"value": GLOBAL_BATCH * args.steps / (ms_e2e / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * world, "ms_per_step": ms_e2e / args.steps,
+               "final_loss": float(loss_host[(args.steps - 1) % loss_host.numel()])}
+
+    nvl, hbm = xchg.layer_bytes(L_DOM)
+    avg = statistics.mean(durs) if durs else None
+    roof = None
+    if avg:
+        ach = hbm / (avg / 1e3) / 1e9
+        peak, peak_src = hbm_peak()
+        roof = {"bound": "hbm", "kernel": "k_twoshot (fc6 fold + fused momentum update%s)" %
+                (" + RS/AG peer stores" if world > 1 else ""), "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": None, "algorithmic_bytes_per_launch": hbm,
+                "avg_launch_ms_in_step": avg, "peak_source": peak_src,
+                "launch_share_of_step": (avg * 1) / (ms / args.steps)}
+        if iso:
+            roof["isolated_launch_ms"] = statistics.median(iso)
+            roof["isolated_achieved"] = hbm / (statistics.median(iso) / 1e3) / 1e9
+            roof["isolated_frac"] = roof["isolated_achieved"] / peak
+    line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
+            "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
+            "gpu_launches": launches, "e2e": e2e}
+    if world > 1 and avg:
+        line["roofline_nvlink"] = {"bound": "nvlink", "achieved": nvl / (avg / 1e3) / 1e9, "peak": NVLINK_PEAK_GBS,
+                                   "unit": "GB/s", "frac": nvl / (avg / 1e3) / 1e9 / NVLINK_PEAK_GBS,
+                                   "bytes_per_launch": nvl, "peak_source": "B200_PROFILING.md measured peer copy"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_step_timing(world, seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if tr.device_status() != 0:
+        raise SystemExit(f"device status {tr.device_status()} (timeout in a device wait)")
+    xchg.close()
+    tr.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback B200_PROFILING.md 6.65 TB/s"
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        pgx_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -196,6 +196,8 @@ int pgx_xchg_layer(pgx_xchg* x, int layer, uint32_t iteration, const void* const
  * this rank's model buffer (forward-pre-hook gate, replaces
  * finalize_iteration's global drain, pipelined.py:60-80). */
 int pgx_xchg_gate(pgx_xchg* x, int layer, uint32_t iteration, void* stream);
+/* Kernels this exchange object has launched so far (exchange + gate kernels). */
+int pgx_xchg_launch_count(pgx_xchg* x, uint64_t* count_out);
 /* Per-layer launch statistics for the roofline (bytes moved per launch). */
 int pgx_xchg_layer_bytes(pgx_xchg* x, int layer, uint64_t* nvlink_out_bytes,
                          uint64_t* hbm_bytes);

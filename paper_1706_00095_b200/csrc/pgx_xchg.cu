@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
     if (threadIdx.x < (unsigned)nc) s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)threadIdx.x * a.C + c;
     __syncthreads();
     cta_wait_flags(s_flags, nc, a.epoch, a.st);
-    const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.S;
+    const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl;
     uint64_t nvec = (hi - lo + W - 1) / W;
     for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
       uint64_t e = lo + q * W;
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
       grad_vec<T>(a.g, e, cnt, acc);
       for (int s = 0; s < nc; ++s) {
         T x[W];
-        ld_vec<T>(rxb + (uint64_t)s * a.S + e, cnt, x);
+        ld_vec<T>(rxb + (uint64_t)s * a.sl + e, cnt, x);
 #pragma unroll
         for (int k = 0; k < W; ++k) {
           if constexpr (sizeof(T) == 8)
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
         st_vec<T>(wp, cnt, w);
         for (int s = 0; s < nc; ++s) st_vec<T>(static_cast<T*>(a.model[tree_child(0, s)]) + e, cnt, w);
       } else {
-        T* dst = static_cast<T*>(a.rx[parent]) + ((uint64_t)(a.parity * a.K + myslot) * a.S + e);
+        T* dst = static_cast<T*>(a.rx[parent]) + ((uint64_t)(a.parity * a.K + myslot) * a.sl + e);
         st_vec<T>(dst, cnt, acc);
       }
     }
@@ -426,6 +426,7 @@ struct pgx_xchg {
   void* peer_rx[PGX_MAX_RANKS] = {};
   uint32_t* peer_rxflags[PGX_MAX_RANKS] = {};
   bool connected = false;
+  uint64_t launches = 0;
   cudaStream_t down = nullptr;
   std::vector<cudaEvent_t> done;
 };
@@ -547,11 +548,11 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
                     (P.S - own) * x->esz;
       (void)my_chunks;
     } else if (P.variant == PGX_VARIANT_TREE) {
-      P.sl = P.S;
+      P.sl = align_up(P.S, kAlignElems);  // slot stride keeps every slot 16B-aligned
       P.C = (uint32_t)((P.S + CH - 1) / CH);
       P.K = std::max(kmax, 1);
       P.rx_off = rxoff;
-      rxoff = align_up(rxoff + 2 * (uint64_t)P.K * P.S, kAlignElems);
+      rxoff = align_up(rxoff + 2 * (uint64_t)P.K * P.sl, kAlignElems);
       P.rxflag_off = rxfoff;
       rxfoff += (uint64_t)P.K * P.C;
       P.dflag = dflag;
@@ -667,6 +668,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
     uint32_t n = a.item_end > a.item_begin ? a.item_end - a.item_begin : 0;
     if (n) {
+      ++x->launches;
       int grid = (int)std::min<uint32_t>(n, (uint32_t)P.grid);
       if (x->esz == 8)
         launch_twoshot<double>(x->world, grid, s, a);
@@ -675,6 +677,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     }
   } else {
     if (phases & PGX_PHASE_PUSH) {
+      ++x->launches;
       a.item_begin = 0;
       a.item_end = P.items;
       if (x->esz == 8)
@@ -692,6 +695,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
       // up passes are not queued behind it (host-stepped callers pass PUSH and
       // DOWN separately and get the down pass on `stream`)
       cudaStream_t ds = (phases & PGX_PHASE_PUSH) ? x->down : s;
+      ++x->launches;
       if (x->esz == 8)
         k_tree_down<double><<<P.down_grid, kThreads, 0, ds>>>(d);
       else
@@ -714,11 +718,17 @@ int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
   if (prev != x->dev) cudaSetDevice(x->dev);
   cudaError_t e = cudaStreamWaitEvent(s, x->done[l], 0);
   if (e == cudaSuccess && P.expected) {
+    ++x->launches;
     k_gate<<<1, 32, 0, s>>>(x->mflags + l, (iteration + 1) * P.expected, world_status(x->w));
     e = cudaGetLastError();
   }
   if (prev != x->dev) cudaSetDevice(prev);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "gate failed: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
+int pgx_xchg_launch_count(pgx_xchg* x, uint64_t* n) {
+  *n = x->launches;
   return PGX_OK;
 }
 

@@ -113,6 +113,12 @@ class DeviceExchange:
         _lib.call("pgx_xchg_layer", self.handle, layer, iteration & 0xFFFFFFFF, ptrs, cnts, n, phases, s)
         self.launches += 1
 
+    def launch_count(self) -> int:
+        """Kernels launched by this exchange so far (exchange + gate kernels)."""
+        n = C.c_uint64()
+        _lib.call("pgx_xchg_launch_count", self.handle, C.byref(n))
+        return n.value
+
     def gate(self, layer: int, iteration: int, stream=None) -> None:
         """Make `stream` (default: current) wait for layer's weights of `iteration`."""
         s = stream if stream is not None else torch.cuda.current_stream(self.tr.device)
@@ -158,6 +164,8 @@ class ModuleBinding:
                 self._handles.append(p.register_post_accumulate_grad_hook(self._make_hook(l)))
             self._handles.append(mod.register_forward_pre_hook(self._make_gate(l)))
         self.gpu_launches = 0
+        self.timed_layers: set = set()   # layers whose launches are bracketed by CUDA events
+        self.events: dict = {}
 
     def _make_hook(self, l):
         def hook(_p):
@@ -175,7 +183,15 @@ class ModuleBinding:
                     g = g.contiguous()
                 g.record_stream(self.x.stream)
                 pieces.append(g)
+            timed = l in self.timed_layers
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(self.x.stream)
             self.x.launch(l, self.k, pieces)
+            if timed:
+                e1.record(self.x.stream)
+                self.events.setdefault(l, []).append((e0, e1))
             for p in params:
                 p.grad = None  # next backward allocates fresh gradients; the allocator
                 # keeps these alive until the exchange stream is past them
