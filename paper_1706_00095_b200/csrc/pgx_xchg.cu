@@ -136,14 +136,14 @@ __device__ __forceinline__ void st_vec(T* p, int cnt, const T* in) {
 
 // Fused update of one element (pgx_mode), identical to pgx_ops.cu / the oracle.
 template <class T>
-__device__ __forceinline__ T apply_update(T w, T g, float* v, const XArgs& a) {
+__device__ __forceinline__ T apply_update(T w, T g, float& v, const XArgs& a) {
   if constexpr (sizeof(T) == 8) {
     return __dsub_rn(w, __dmul_rn(a.lr, g));
   } else {
     if (a.mode == PGX_MODE_REF32) return __double2float_rn(__dsub_rn((double)w, __dmul_rn(a.lr, (double)g)));
     float gg = __fadd_rn(__fmul_rn(a.scale, g), __fmul_rn(a.wd, w));
-    float vv = __fadd_rn(__fmul_rn(a.mu, *v), __fmul_rn((float)a.lr, gg));
-    *v = vv;
+    float vv = __fadd_rn(__fmul_rn(a.mu, v), __fmul_rn((float)a.lr, gg));
+    v = vv;
     return __fsub_rn(w, vv);
   }
 }
@@ -156,13 +156,67 @@ __device__ __forceinline__ void update_vec(T* w, const T* g, float* v, int cnt, 
       float vv[W];
       ld_vec<float>(v, cnt, vv);
 #pragma unroll
-      for (int k = 0; k < W; ++k) w[k] = apply_update<T>(w[k], g[k], &vv[k], a);
+      for (int k = 0; k < W; ++k) w[k] = apply_update<T>(w[k], g[k], vv[k], a);
       st_vec<float>(v, cnt, vv);
       return;
     }
   }
+  float dummy = 0.f;
 #pragma unroll
-  for (int k = 0; k < W; ++k) w[k] = apply_update<T>(w[k], g[k], nullptr, a);
+  for (int k = 0; k < W; ++k) w[k] = apply_update<T>(w[k], g[k], dummy, a);
+}
+
+// Owner work on U vectors per thread: all loads first (U*(N+2) 16-byte requests in
+// flight), then tree-order fold, fused update, local + peer stores.
+template <int N, class T, int U>
+__device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint64_t lo, uint64_t hi,
+                                              uint64_t q0, uint64_t nvec) {
+  constexpr int W = VecT<T>::W;
+  const int me = a.rank;
+  const bool fast = sizeof(T) == 4 && a.mode == PGX_MODE_FAST32;
+  T vals[U][N][W];
+  T w[U][W];
+  float vv[U][W];
+  int cnt[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    uint64_t q = q0 + (uint64_t)u * blockDim.x;
+    uint64_t e = lo + q * W;
+    cnt[u] = q < nvec ? (int)min((uint64_t)W, hi - e) : 0;
+    if (cnt[u] > 0) {
+#pragma unroll
+      for (int s = 0; s < N; ++s) {
+        if (s == me)
+          grad_vec<T>(a.g, e, cnt[u], vals[u][s]);
+        else
+          ld_vec<T>(rxb + (uint64_t)s * a.sl + q * W, cnt[u], vals[u][s]);
+      }
+      ld_vec<T>(static_cast<const T*>(a.model[me]) + e, cnt[u], w[u]);
+      if (fast) ld_vec<float>(a.v + e, cnt[u], vv[u]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (cnt[u] <= 0) continue;
+    uint64_t e = lo + (q0 + (uint64_t)u * blockDim.x) * W;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      T col[N];
+#pragma unroll
+      for (int s = 0; s < N; ++s) col[s] = vals[u][s][k];
+      T g;
+      if constexpr (sizeof(T) == 8)
+        g = tree_sum<N>(col, AddF64{});
+      else
+        g = tree_sum<N>(col, AddF32{});
+      w[u][k] = apply_update<T>(w[u][k], g, vv[u][k], a);
+    }
+    st_vec<T>(static_cast<T*>(a.model[me]) + e, cnt[u], w[u]);
+    if (fast) st_vec<float>(a.v + e, cnt[u], vv[u]);
+#pragma unroll
+    for (int s = 0; s < N; ++s)
+      if (s != me) st_vec<T>(static_cast<T*>(a.model[s]) + e, cnt[u], w[u]);
+  }
 }
 
 // One thread raises a flag / counter on a peer after the CTA's payload stores.
@@ -221,12 +275,20 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
       if (lo < hi) {
         T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * a.sl + (lo - j * a.sl));
         uint64_t nvec = (hi - lo + W - 1) / W;
-        for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
-          uint64_t e = lo + q * W;
-          int cnt = (int)min((uint64_t)W, hi - e);
-          T buf[W];
-          grad_vec<T>(a.g, e, cnt, buf);
-          st_vec<T>(dst + q * W, cnt, buf);
+        constexpr int UP = 4;
+        for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)UP * blockDim.x) {
+          T buf[UP][W];
+          int cnt[UP];
+#pragma unroll
+          for (int u = 0; u < UP; ++u) {
+            uint64_t q = q0 + (uint64_t)u * blockDim.x;
+            uint64_t e = lo + q * W;
+            cnt[u] = q < nvec ? (int)min((uint64_t)W, hi - e) : 0;
+            if (cnt[u] > 0) grad_vec<T>(a.g, e, cnt[u], buf[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < UP; ++u)
+            if (cnt[u] > 0) st_vec<T>(dst + (q0 + (uint64_t)u * blockDim.x) * W, cnt[u], buf[u]);
         }
         cta_release_flag(a.rxflags[j] + (uint64_t)me * a.C + c, a.epoch);
       }
@@ -244,37 +306,9 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
       cta_wait_flags(s_flags, N - 1, a.epoch, a.st);
       const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl + (lo - me * a.sl);
       uint64_t nvec = (hi - lo + W - 1) / W;
-      for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
-        uint64_t e = lo + q * W;
-        int cnt = (int)min((uint64_t)W, hi - e);
-        T vals[N][W];
-#pragma unroll
-        for (int s = 0; s < N; ++s) {
-          if (s == me)
-            grad_vec<T>(a.g, e, cnt, vals[s]);
-          else
-            ld_vec<T>(rxb + (uint64_t)s * a.sl + q * W, cnt, vals[s]);
-        }
-        T* wp = static_cast<T*>(a.model[me]) + e;
-        T w[W];
-        ld_vec<T>(wp, cnt, w);
-        T g[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-          T col[N];
-#pragma unroll
-          for (int s = 0; s < N; ++s) col[s] = vals[s][k];
-          if constexpr (sizeof(T) == 8)
-            g[k] = tree_sum<N>(col, AddF64{});
-          else
-            g[k] = tree_sum<N>(col, AddF32{});
-        }
-        update_vec<T>(w, g, a.v ? a.v + e : nullptr, cnt, a);
-        st_vec<T>(wp, cnt, w);
-#pragma unroll
-        for (int s = 0; s < N; ++s)
-          if (s != me) st_vec<T>(static_cast<T*>(a.model[s]) + e, cnt, w);
-      }
+      constexpr int U = N <= 4 ? 2 : 1;
+      for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
+        owner_vectors<N, T, U>(a, rxb, lo, hi, q0, nvec);
       __syncthreads();
       if (threadIdx.x < N - 1) {
         int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
@@ -474,11 +508,28 @@ XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
   return a;
 }
 
+// Grid = min(requested, resident CTAs): CTAs beyond what fits only spin up to
+// find the queue empty.
+template <int N, class T>
+int resident_grid(int want, int dev) {
+  static int cap = 0;  // per instantiation; one device model per process
+  if (!cap) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_twoshot<N, T>, kThreads, 0);
+    cap = std::max(1, per_sm) * sm_count(dev);
+  }
+  return std::max(1, std::min(want, cap));
+}
+
 template <class T>
-void launch_twoshot(int N, dim3 g, cudaStream_t s, const XArgs& a) {
+void launch_twoshot(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
   switch (N) {
-#define PGX_CASE(n) \
-  case n: k_twoshot<n, T><<<g, kThreads, 0, s>>>(a); break;
+#define PGX_CASE(n)                                                    \
+  case n: {                                                            \
+    int g = resident_grid<n, T>(want, dev);                            \
+    k_twoshot<n, T><<<g, kThreads, 0, s>>>(a);                         \
+    break;                                                             \
+  }
     PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
 #undef PGX_CASE
   }
@@ -540,7 +591,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
         remote += (uint32_t)((hi - lo + CH - 1) / CH);
       }
       P.expected = remote;
-      P.grid = (int)std::min<uint64_t>(P.items, cap);
+      P.grid = (int)std::min<uint64_t>(P.items, cfg->max_ctas > 0 ? cap : (N == 1 ? 4 * sms : cap));
       uint64_t own = my_hi - my_lo;
       P.nvlink_bytes = (N > 1) ? 2ull * (P.S - own) * x->esz : 0;  // RS out + AG out
       // owner fold: N partial reads + w (+v) read/write; pushes read the rest of the gradient
@@ -671,9 +722,9 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
       ++x->launches;
       int grid = (int)std::min<uint32_t>(n, (uint32_t)P.grid);
       if (x->esz == 8)
-        launch_twoshot<double>(x->world, grid, s, a);
+        launch_twoshot<double>(x->world, grid, x->dev, s, a);
       else
-        launch_twoshot<float>(x->world, grid, s, a);
+        launch_twoshot<float>(x->world, grid, x->dev, s, a);
     }
   } else {
     if (phases & PGX_PHASE_PUSH) {
