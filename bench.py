@@ -38,13 +38,15 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    p.add_argument("--variant", default="twoshot", choices=["twoshot", "tree", "auto"])
+    p.add_argument("--variant", default="twoshot", choices=["twoshot", "tree", "twoshot_ce", "auto"])
     p.add_argument("--chunk-elems", type=int, default=16384)
     p.add_argument("--max-ctas", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--timeline", default="")
+    p.add_argument("--per-gpu-batch", type=int, default=0,
+                   help="diagnostic only: override 256/N (the line is then not the headline config)")
     return p.parse_args()
 
 
@@ -256,7 +258,8 @@ def pgx_arm(args):
     tr.barrier()      # rendezvous: every rank's segments attached over CUDA IPC
     xchg.connect()
 
-    B = GLOBAL_BATCH // world
+    B = args.per_gpu_batch or GLOBAL_BATCH // world
+    gb = B * world  # images per step, whole job
     g = torch.Generator().manual_seed(42 + rank)
     host_x = torch.randint(0, 256, (B, 3, 227, 227), dtype=torch.uint8, generator=g).pin_memory()
     host_y = torch.randint(0, 1000, (B,), dtype=torch.int64, generator=g).pin_memory()
@@ -313,7 +316,7 @@ def pgx_arm(args):
     clk = clocks.stop()
     durs = [a.elapsed_time(b) for a, b in bind.events.get(L_DOM, [])]
     bind.timed_layers = set()
-    value = GLOBAL_BATCH * args.steps / (ms / 1e3)
+    value = gb * args.steps / (ms / 1e3)
 
     # ---- dominant kernel in isolation (same launch, no concurrent backward) ----
     gfc6 = [torch.randn(4096, 9216, device=dev) * 1e-3, torch.randn(4096, device=dev) * 1e-3]
@@ -338,7 +341,7 @@ def pgx_arm(args):
             loss_host[i % loss_host.numel()].copy_(loss.detach(), non_blocking=True)
         ms_e2e = timed(e2e_step, args.steps)
         h2d = (host_x.numel() * host_x.element_size() + host_y.numel() * host_y.element_size()) * world
-        e2e = {"value": GLOBAL_BATCH * args.steps / (ms_e2e / 1e3), "unit": "images/s",
+        e2e = {"value": gb * args.steps / (ms_e2e / 1e3), "unit": "images/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * world, "ms_per_step": ms_e2e / args.steps,
                "final_loss": float(loss_host[(args.steps - 1) % loss_host.numel()])}
 
@@ -362,6 +365,10 @@ def pgx_arm(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
             "gpu_launches": launches, "e2e": e2e}
+    if args.per_gpu_batch:
+        line["config"]["per_gpu_batch"] = B
+        line["config"]["global_batch"] = gb
+        line["config"]["diagnostic"] = "per-GPU batch overridden; not the headline configuration"
     if world > 1 and avg:
         line["roofline_nvlink"] = {"bound": "nvlink", "achieved": nvl / (avg / 1e3) / 1e9, "peak": NVLINK_PEAK_GBS,
                                    "unit": "GB/s", "frac": nvl / (avg / 1e3) / 1e9 / NVLINK_PEAK_GBS,

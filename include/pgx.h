@@ -157,7 +157,11 @@ int pgx_seeded_fill_f32(uint64_t seed, double scale, float* out, uint64_t n, voi
  *                                  owner fold (same tree order) + fused update,
  *                                  one-sided all-gather into peers' weights.
  * Both are bit-identical to the reference fold order. */
-enum pgx_variant { PGX_VARIANT_TREE = 0, PGX_VARIANT_TWOSHOT = 1 };
+enum pgx_variant {
+  PGX_VARIANT_TREE = 0,       /* paper: binomial reduce + master update + broadcast     */
+  PGX_VARIANT_TWOSHOT = 1,    /* SM peer stores: reduce-scatter, owner update, gather   */
+  PGX_VARIANT_TWOSHOT_CE = 2  /* same schedule, shards moved by the copy engines        */
+};
 
 typedef struct pgx_xchg_config {
   int num_layers;
@@ -196,6 +200,11 @@ int pgx_xchg_layer(pgx_xchg* x, int layer, uint32_t iteration, const void* const
  * this rank's model buffer (forward-pre-hook gate, replaces
  * finalize_iteration's global drain, pipelined.py:60-80). */
 int pgx_xchg_gate(pgx_xchg* x, int layer, uint32_t iteration, void* stream);
+/* Internal streams (0 = tree down pass, 1 = CE reduce-scatter, 2 = CE owner side),
+ * so callers can tie gradient lifetimes to them. */
+int pgx_xchg_stream(pgx_xchg* x, int which, void** stream_out);
+/* Make `stream` wait until layer l's local exchange work (own shard) finished. */
+int pgx_xchg_join(pgx_xchg* x, int layer, void* stream);
 /* Kernels this exchange object has launched so far (exchange + gate kernels). */
 int pgx_xchg_launch_count(pgx_xchg* x, uint64_t* count_out);
 /* Per-layer launch statistics for the roofline (bytes moved per launch). */

@@ -23,7 +23,7 @@ MAX_RANKS = 8
 MAX_PIECES = 4
 
 MODE_REF64, MODE_REF32, MODE_FAST32 = 0, 1, 2
-VARIANT_TREE, VARIANT_TWOSHOT = 0, 1
+VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE = 0, 1, 2
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p
@@ -87,6 +87,8 @@ SIGNATURES = {
     "pgx_xchg_gate": [vp, i32, u32, vp],
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
     "pgx_xchg_launch_count": [vp, P(u64)],
+    "pgx_xchg_stream": [vp, i32, P(vp)],
+    "pgx_xchg_join": [vp, i32, vp],
 }
 _RESTYPE = {"pgx_last_error": C.c_char_p}
 

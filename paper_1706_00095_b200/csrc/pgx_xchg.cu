@@ -20,6 +20,7 @@
 // into chunks (the notification unit, runtime.py:209-222) claimed through a
 // per-layer atomic queue: every non-waiting push chunk is claimed before any
 // waiting chunk, so a launch makes progress with any number of resident CTAs.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <string.h>
 
@@ -168,7 +169,7 @@ __device__ __forceinline__ void update_vec(T* w, const T* g, float* v, int cnt, 
 
 // Owner work on U vectors per thread: all loads first (U*(N+2) 16-byte requests in
 // flight), then tree-order fold, fused update, local + peer stores.
-template <int N, class T, int U>
+template <int N, class T, int U, bool kRemote = true>
 __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint64_t lo, uint64_t hi,
                                               uint64_t q0, uint64_t nvec) {
   constexpr int W = VecT<T>::W;
@@ -213,9 +214,11 @@ __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint
     }
     st_vec<T>(static_cast<T*>(a.model[me]) + e, cnt[u], w[u]);
     if (fast) st_vec<float>(a.v + e, cnt[u], vv[u]);
+    if constexpr (kRemote) {
 #pragma unroll
-    for (int s = 0; s < N; ++s)
-      if (s != me) st_vec<T>(static_cast<T*>(a.model[s]) + e, cnt[u], w[u]);
+      for (int s = 0; s < N; ++s)
+        if (s != me) st_vec<T>(static_cast<T*>(a.model[s]) + e, cnt[u], w[u]);
+    }
   }
 }
 
@@ -426,6 +429,32 @@ __global__ void k_gate(const uint32_t* counter, uint32_t want, Status st) {
   if (threadIdx.x == 0) wait_geq(counter, want, st);
 }
 
+// Copy-engine two-shot (TWOSHOT_CE): the gradient shards and the updated shards
+// travel as peer DMA copies (the GPU's copy engines are the RDMA engine of a
+// GPI-2 write_notify: one-sided and without compute resources); each transfer is
+// followed by a fenced stream write of the notification.  SMs only run the local
+// fold + update below and these bounded flag waits.
+struct FlagSet {
+  const uint32_t* f[PGX_MAX_RANKS];
+  int n;
+};
+__global__ void k_wait_flags(FlagSet fs, uint32_t want, Status st) {
+  if (threadIdx.x < (unsigned)fs.n) wait_geq(fs.f[threadIdx.x], want, st);
+}
+
+template <int N, class T>
+__global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
+  constexpr int W = VecT<T>::W;
+  constexpr int U = N <= 4 ? 2 : 1;
+  const int me = a.rank;
+  uint64_t lo = min((uint64_t)me * a.sl, a.S), hi = min((uint64_t)(me + 1) * a.sl, a.S);
+  if (lo >= hi) return;
+  const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl;
+  const uint64_t nvec = (hi - lo + W - 1) / W, span = (uint64_t)U * blockDim.x;
+  for (uint64_t blk = blockIdx.x; blk * span < nvec; blk += gridDim.x)
+    owner_vectors<N, T, U, false>(a, rxb, lo, hi, blk * span + threadIdx.x, nvec);
+}
+
 struct LayerPlan {
   uint64_t S = 0;
   int variant = 0;
@@ -462,7 +491,10 @@ struct pgx_xchg {
   bool connected = false;
   uint64_t launches = 0;
   cudaStream_t down = nullptr;
+  cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
   std::vector<cudaEvent_t> done;
+  std::vector<cudaEvent_t> ready;                  // TWOSHOT_CE: gradient ready on the launch stream
+  uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
 };
 
 namespace {
@@ -535,7 +567,100 @@ void launch_twoshot(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
   }
 }
 
+template <class T>
+void launch_owner_local(int N, int grid, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n) \
+  case n: k_owner_local<n, T><<<grid, kThreads, 0, s>>>(a); break;
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
 }  // namespace
+
+// cuStreamWriteValue32 through the runtime's driver entry point, so libpgx.so does
+// not link libcuda (it must load on machines without a driver).
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
+  }
+  return fn;
+}
+
+// TWOSHOT_CE launch: reduce-scatter and all-gather as peer DMA copies + fenced
+// stream writes of the notifications; owner fold/update as a local kernel.
+static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, cudaStream_t s, int phases) {
+  const int N = x->world, me = x->rank;
+  const int esz = x->esz;
+  cudaError_t e = cudaEventRecord(x->ready[l], s);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
+  if (phases & PGX_PHASE_PUSH) {
+    cudaStreamWaitEvent(x->ce_rs, x->ready[l], 0);
+    for (int d = 1; d < N; ++d) {
+      int j = (me + d) % N;
+      uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
+      uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * P.sl) * esz;
+      uint64_t pb = 0;
+      for (int k = 0; k < a.g.n && lo < hi; ++k) {
+        uint64_t pe = a.g.end[k];
+        uint64_t ol = std::max(lo, pb), oh = std::min(hi, pe);
+        if (ol < oh) {
+          e = cudaMemcpyAsync(dst + (ol - lo) * esz, static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz,
+                              (oh - ol) * esz, cudaMemcpyDeviceToDevice, x->ce_rs);
+          if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
+        }
+        pb = pe;
+      }
+      WriteValue32Fn wv = write_value32();
+      if (!wv) return fail(PGX_E_CUDA, "cuStreamWriteValue32 entry point unavailable");
+      CUresult cr = wv((CUstream)x->ce_rs, (CUdeviceptr)(a.rxflags[j] + (uint64_t)me * P.C),
+                                         a.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+      if (cr != CUDA_SUCCESS) return fail(PGX_E_CUDA, "cuStreamWriteValue32 failed (%d)", (int)cr);
+    }
+  }
+  if (phases & PGX_PHASE_OWNER) {
+    cudaStreamWaitEvent(x->ce_own, x->ready[l], 0);
+    FlagSet fs{};
+    fs.n = 0;
+    for (int sidx = 0; sidx < N; ++sidx)
+      if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C;
+    if (fs.n) {
+      k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.st);
+      ++x->launches;
+    }
+    int grid = std::max(1, std::min(P.grid, (int)((P.sl / VecT<float>::W + kThreads - 1) / kThreads)));
+    if (esz == 8)
+      launch_owner_local<double>(N, grid, x->ce_own, a);
+    else
+      launch_owner_local<float>(N, grid, x->ce_own, a);
+    ++x->launches;
+    uint64_t lo = std::min(P.S, (uint64_t)me * P.sl), hi = std::min(P.S, (uint64_t)(me + 1) * P.sl);
+    for (int d = 1; d < N; ++d) {
+      int t = (me + d) % N;
+      if (lo < hi) {
+        e = cudaMemcpyAsync(static_cast<uint8_t*>(a.model[t]) + lo * esz, static_cast<uint8_t*>(a.model[me]) + lo * esz,
+                            (hi - lo) * esz, cudaMemcpyDeviceToDevice, x->ce_own);
+        if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
+      }
+      WriteValue32Fn wv = write_value32();
+      if (!wv) return fail(PGX_E_CUDA, "cuStreamWriteValue32 entry point unavailable");
+      CUresult cr = wv((CUstream)x->ce_own,
+                                         (CUdeviceptr)(a.mflags[t] + x->ownerflag_base + (uint64_t)l * N + me),
+                                         a.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+      if (cr != CUDA_SUCCESS) return fail(PGX_E_CUDA, "cuStreamWriteValue32 failed (%d)", (int)cr);
+    }
+    e = cudaEventRecord(x->done[l], x->ce_own);
+    if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
+  }
+  return PGX_OK;
+}
 
 extern "C" {
 
@@ -572,7 +697,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     P.variant = cfg->variant ? cfg->variant[l] : PGX_VARIANT_TWOSHOT;
     P.model_off = moff;
     moff = align_up(moff + P.S, kAlignElems);
-    if (P.variant == PGX_VARIANT_TWOSHOT) {
+    if (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CE) {
       P.sl = align_up((P.S + N - 1) / N, 4);
       P.C = (uint32_t)((P.sl + CH - 1) / CH);
       P.K = N;
@@ -625,6 +750,8 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   }
   int rc;
   // model segment: flat weights + [arrival counters | tree down flags]
+  x->ownerflag_base = dflag;
+  dflag += (uint32_t)cfg->num_layers * N;  // TWOSHOT_CE per-(layer, owner) arrival flags
   rc = pgx_segment_create(w, x->seg_model, std::max<uint64_t>(moff, 1) * x->esz, dflag, &x->model, &x->mflags);
   if (rc) { delete x; return rc; }
   rc = pgx_segment_create(w, x->seg_rx, std::max<uint64_t>(rxoff, 1) * x->esz, (uint32_t)std::max<uint64_t>(rxfoff, 1),
@@ -644,9 +771,14 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->down, cudaStreamNonBlocking, hi_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs, cudaStreamNonBlocking, hi_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_own, cudaStreamNonBlocking, hi_prio);
     x->done.resize(cfg->num_layers);
-    for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l)
+    x->ready.resize(cfg->num_layers);
+    for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l) {
       e = cudaEventCreateWithFlags(&x->done[l], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ready[l], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -667,7 +799,10 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   if (x->v) cudaFree(x->v);
   if (x->queues) cudaFree(x->queues);
   for (auto e : x->done) cudaEventDestroy(e);
+  for (auto e : x->ready) cudaEventDestroy(e);
   if (x->down) cudaStreamDestroy(x->down);
+  if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
+  if (x->ce_own) cudaStreamDestroy(x->ce_own);
   cudaSetDevice(prev);
   delete x;  // segments belong to the world
   return PGX_OK;
@@ -714,6 +849,11 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
   int prev;
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
+  if (P.variant == PGX_VARIANT_TWOSHOT_CE) {
+    int rc = launch_twoshot_ce(x, l, P, a, s, phases);
+    if (prev != x->dev) cudaSetDevice(prev);
+    return rc;
+  }
   if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
@@ -768,13 +908,40 @@ int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
   cudaError_t e = cudaStreamWaitEvent(s, x->done[l], 0);
-  if (e == cudaSuccess && P.expected) {
+  if (e == cudaSuccess && P.variant == PGX_VARIANT_TWOSHOT_CE) {
+    FlagSet fs{};
+    for (int j = 0; j < x->world; ++j) {
+      if (j == x->rank) continue;
+      uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
+      (void)lo;
+      (void)hi;
+      fs.f[fs.n++] = x->mflags + x->ownerflag_base + (uint64_t)l * x->world + j;
+    }
+    if (fs.n) {
+      ++x->launches;
+      k_wait_flags<<<1, 32, 0, s>>>(fs, iteration + 1, world_status(x->w));
+      e = cudaGetLastError();
+    }
+  } else if (e == cudaSuccess && P.expected) {
     ++x->launches;
     k_gate<<<1, 32, 0, s>>>(x->mflags + l, (iteration + 1) * P.expected, world_status(x->w));
     e = cudaGetLastError();
   }
   if (prev != x->dev) cudaSetDevice(prev);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "gate failed: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
+int pgx_xchg_stream(pgx_xchg* x, int which, void** out) {
+  cudaStream_t st[3] = {x->down, x->ce_rs, x->ce_own};
+  if (which < 0 || which > 2) return fail(PGX_E_RANGE, "stream index %d outside 0..2", which);
+  *out = st[which];
+  return PGX_OK;
+}
+
+int pgx_xchg_join(pgx_xchg* x, int l, void* stream) {
+  if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
+  PGX_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, x->done[l], 0));
   return PGX_OK;
 }
 

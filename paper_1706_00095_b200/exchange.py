@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from .errors import ConfigError, ShapeError
 
-VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT}
+VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32}
 
 
@@ -83,6 +83,11 @@ class DeviceExchange:
             self.stream = torch.cuda.Stream(device=transport.device, priority=-1)
         self.connected = False
         self.launches = 0
+        self.internal_streams = []
+        for which in range(3):
+            sp = C.c_void_p()
+            _lib.call("pgx_xchg_stream", h, which, C.byref(sp))
+            self.internal_streams.append(torch.cuda.ExternalStream(sp.value, device=transport.device))
 
     # -- wiring ----------------------------------------------------------------
     def connect(self) -> None:
@@ -112,6 +117,10 @@ class DeviceExchange:
         s = (stream or self.stream).cuda_stream
         _lib.call("pgx_xchg_layer", self.handle, layer, iteration & 0xFFFFFFFF, ptrs, cnts, n, phases, s)
         self.launches += 1
+
+    def join(self, layer: int, stream) -> None:
+        """Make `stream` wait until this rank's part of layer's last exchange is done."""
+        _lib.call("pgx_xchg_join", self.handle, layer, stream.cuda_stream)
 
     def launch_count(self) -> int:
         """Kernels launched by this exchange so far (exchange + gate kernels)."""
@@ -182,6 +191,8 @@ class ModuleBinding:
                 if not g.is_contiguous():
                     g = g.contiguous()
                 g.record_stream(self.x.stream)
+                for st in self.x.internal_streams:  # copy-engine variants read it there
+                    g.record_stream(st)
                 pieces.append(g)
             timed = l in self.timed_layers
             if timed:

@@ -96,7 +96,7 @@ def _ngpu():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["twoshot", "tree"])
+@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce"])
 @pytest.mark.parametrize("mode", ["ref32", "fast32"])
 def test_concurrent_exchange_matches_oracle(variant, mode):
     out = _spawn(_exchange_worker, _ngpu(), variant, mode)

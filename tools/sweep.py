@@ -30,7 +30,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=16384)
-    ap.add_argument("--variants", default="twoshot,tree,nccl")
+    ap.add_argument("--variants", default="twoshot,twoshot_ce,tree,nccl")
     ap.add_argument("--mode", default="fast32")
     args = ap.parse_args()
 
@@ -56,7 +56,7 @@ def main():
     xs = {}
     seg = 16
     for v in variants:
-        if v in ("twoshot", "tree"):
+        if v in ("twoshot", "tree", "twoshot_ce"):
             xs[v] = DeviceExchange(tr, elems, mode=args.mode, variant=v, chunk_elems=args.chunk, lr=0.01,
                                    momentum=0.9, weight_decay=5e-4, seg_base=seg, max_ctas=args.ctas)
             seg += 2
@@ -86,6 +86,7 @@ def main():
                     k = it + 1000 * 0
                     e0.record(x.stream)
                     x.launch(li, k + li * 0, [g])
+                    x.join(li, x.stream)
                     x.gate(li, k, stream=x.stream)
                     e1.record(x.stream)
                 torch.cuda.synchronize()
