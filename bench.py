@@ -42,6 +42,7 @@ def parse():
     p.add_argument("--chunk-elems", type=int, default=16384)
     p.add_argument("--max-ctas", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="eager steps instead of a captured CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--timeline", default="")
@@ -133,7 +134,7 @@ def workload_config(world, args):
             "parallelism": f"dp{world}", "exchange": args.variant, "update": "fast32 momentum SGD lr 0.01 mu 0.9 "
             "wd 5e-4 scale 1/N", "fwd_bwd": "PyTorch cuDNN bf16 autocast, fp32 master weights/grads",
             "l2": "working set > L2 (244 MB fp32 weights + 244 MB grads + activations per step)",
-            "chunk_elems": args.chunk_elems}
+            "chunk_elems": args.chunk_elems, "step": "CUDA graph replay" if not args.no_graph else "eager"}
 
 
 # ------------------------------------------------------------------ model
@@ -303,20 +304,96 @@ def pgx_arm(args):
         step(dev_x, dev_y)
     bind.drain()
     torch.cuda.synchronize()
+    L_DOM = 5  # fc6: the dominant exchange/update kernel (37.75M params)
+
+    # ---- capture one training step as a CUDA graph (epochs from the device counter) ----
+    graph = None
+    if not args.no_graph:
+        k_before_capture = bind.k
+        xchg.set_device_iteration(True, bind.k - 1)
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream())
+        c0 = xchg.launch_count()
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                bind.begin_step()
+                static_loss = step(dev_x, dev_y)
+                bind.drain()  # joins every exchange stream back into the capture
+        per_step_launches = xchg.launch_count() - c0
+        torch.cuda.current_stream().wait_stream(cap)
+        torch.cuda.synchronize()
+        replays = [0]
+
+        def run_step(xb=None, yb=None):
+            if xb is not None:
+                dev_x.copy_(xb, non_blocking=True)
+                dev_y.copy_(yb, non_blocking=True)
+            graph.replay()
+            replays[0] += 1
+            return static_loss
+
+        def finish():
+            bind.wait_current()
+    else:
+        def run_step(xb=None, yb=None):
+            return step(dev_x if xb is None else xb, dev_y if yb is None else yb)
+
+        def finish():
+            bind.drain()
+
+    def timed(fn, k):
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(k):
+            fn(i)
+        finish()  # the last iteration's weights are installed everywhere
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
 
     # ---- device-resident timed region (value) ----
-    L_DOM = 5  # fc6: the dominant exchange/update kernel (37.75M params)
-    bind.timed_layers = {L_DOM}
-    bind.events.clear()
     clocks = ClockSampler(local)
     clocks.start()
     n0 = xchg.launch_count()
-    ms = timed(lambda i: step(dev_x, dev_y), args.steps)
+    ms = timed(lambda i: run_step(), args.steps)
     launches = xchg.launch_count() - n0
     clk = clocks.stop()
+    if graph is not None:  # launches inside replays are not counted by the host: count one captured step
+        launches = per_step_launches * args.steps
+    value = gb * args.steps / (ms / 1e3)
+
+    # ---- end-to-end through the public API: host batch in, loss out ----
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step(i):
+            loss = run_step(host_x, host_y)
+            loss_host[i % loss_host.numel()].copy_(loss.detach(), non_blocking=True)
+        ms_e2e = timed(e2e_step, args.steps)
+        h2d = (host_x.numel() * host_x.element_size() + host_y.numel() * host_y.element_size()) * world
+        e2e = {"value": gb * args.steps / (ms_e2e / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * world, "ms_per_step": ms_e2e / args.steps,
+               "final_loss": float(loss_host[(args.steps - 1) % loss_host.numel()])}
+
+    # ---- roofline pass: the same steps run eagerly with the fc6 launch bracketed by events ----
+    if graph is not None:
+        torch.cuda.synchronize()
+        bind.k = k_before_capture + replays[0]  # continue the epoch sequence after the replays
+        xchg.set_device_iteration(False, 0)
+    bind.timed_layers = {L_DOM}
+    bind.events.clear()
+    ms_eager = timed(lambda i: step(dev_x, dev_y), args.steps)
     durs = [a.elapsed_time(b) for a, b in bind.events.get(L_DOM, [])]
     bind.timed_layers = set()
-    value = gb * args.steps / (ms / 1e3)
 
     # ---- dominant kernel in isolation (same launch, no concurrent backward) ----
     gfc6 = [torch.randn(4096, 9216, device=dev) * 1e-3, torch.randn(4096, device=dev) * 1e-3]
@@ -326,24 +403,11 @@ def pgx_arm(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(xchg.stream)
             xchg.launch(L_DOM, bind.k + i, gfc6)
+            xchg.join(L_DOM, xchg.stream)
             e1.record(xchg.stream)
             torch.cuda.synchronize()
             iso.append(e0.elapsed_time(e1))
-        bind.k += 10  # keep the epoch sequence monotone (N=1 has no peer flags)
-
-    # ---- end-to-end through the public API: host batch in, loss out ----
-    e2e = None
-    if not args.no_e2e:
-        def e2e_step(i):
-            xb = host_x.to(dev, non_blocking=True)
-            yb = host_y.to(dev, non_blocking=True)
-            loss = step(xb, yb)
-            loss_host[i % loss_host.numel()].copy_(loss.detach(), non_blocking=True)
-        ms_e2e = timed(e2e_step, args.steps)
-        h2d = (host_x.numel() * host_x.element_size() + host_y.numel() * host_y.element_size()) * world
-        e2e = {"value": gb * args.steps / (ms_e2e / 1e3), "unit": "images/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * world, "ms_per_step": ms_e2e / args.steps,
-               "final_loss": float(loss_host[(args.steps - 1) % loss_host.numel()])}
+        bind.k += 10
 
     nvl, hbm = xchg.layer_bytes(L_DOM)
     avg = statistics.mean(durs) if durs else None
@@ -355,7 +419,9 @@ def pgx_arm(args):
                 (" + RS/AG peer stores" if world > 1 else ""), "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": None, "algorithmic_bytes_per_launch": hbm,
                 "avg_launch_ms_in_step": avg, "peak_source": peak_src,
-                "launch_share_of_step": (avg * 1) / (ms / args.steps)}
+                "launch_share_of_step": avg / (ms_eager / args.steps),
+                "measured_in": "eager timed region of %d steps (%.3f ms/step) right after the graph-replay region"
+                % (args.steps, ms_eager / args.steps)}
         if iso:
             roof["isolated_launch_ms"] = statistics.median(iso)
             roof["isolated_achieved"] = hbm / (statistics.median(iso) / 1e3) / 1e9
@@ -364,7 +430,8 @@ def pgx_arm(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
-            "gpu_launches": launches, "e2e": e2e}
+            "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None,
+            "ms_per_step_eager": ms_eager / args.steps}
     if args.per_gpu_batch:
         line["config"]["per_gpu_batch"] = B
         line["config"]["global_batch"] = gb

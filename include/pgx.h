@@ -200,10 +200,19 @@ int pgx_xchg_layer(pgx_xchg* x, int layer, uint32_t iteration, const void* const
  * this rank's model buffer (forward-pre-hook gate, replaces
  * finalize_iteration's global drain, pipelined.py:60-80). */
 int pgx_xchg_gate(pgx_xchg* x, int layer, uint32_t iteration, void* stream);
+/* Graph mode: take the iteration from a device counter instead of the host
+ * argument, so a captured step (CUDA graph) replays with fresh epochs.
+ * `current` = the last iteration already launched (0xFFFFFFFF = none); each
+ * pgx_xchg_tick (captured at the start of a step) advances it by one.  In this
+ * mode pgx_xchg_gate's `iteration` is relative: 0xFFFFFFFF = the previous
+ * iteration (forward-pre-hook gate), 0 = the current one (end-of-step drain). */
+int pgx_xchg_device_iteration(pgx_xchg* x, int enable, uint32_t current);
+int pgx_xchg_tick(pgx_xchg* x, void* stream);
 /* Internal streams (0 = tree down pass, 1 = CE reduce-scatter, 2 = CE owner side),
  * so callers can tie gradient lifetimes to them. */
 int pgx_xchg_stream(pgx_xchg* x, int which, void** stream_out);
-/* Make `stream` wait until layer l's local exchange work (own shard) finished. */
+/* Make `stream` wait until layer l's local exchange work (own shard, side
+ * streams) finished — joins every internal stream back (graph capture). */
 int pgx_xchg_join(pgx_xchg* x, int layer, void* stream);
 /* Kernels this exchange object has launched so far (exchange + gate kernels). */
 int pgx_xchg_launch_count(pgx_xchg* x, uint64_t* count_out);

@@ -89,6 +89,8 @@ SIGNATURES = {
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],
     "pgx_xchg_join": [vp, i32, vp],
+    "pgx_xchg_device_iteration": [vp, i32, u32],
+    "pgx_xchg_tick": [vp, vp],
 }
 _RESTYPE = {"pgx_last_error": C.c_char_p}
 

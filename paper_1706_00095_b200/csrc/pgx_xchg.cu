@@ -20,7 +20,6 @@
 // into chunks (the notification unit, runtime.py:209-222) claimed through a
 // per-layer atomic queue: every non-waiting push chunk is claimed before any
 // waiting chunk, so a launch makes progress with any number of resident CTAs.
-#include <cuda.h>
 #include <cuda_runtime.h>
 #include <string.h>
 
@@ -78,6 +77,7 @@ struct XArgs {
   int rank, world, parity, K;          // K: rx slots per parity
   uint32_t push_items, items;
   uint32_t item_begin, item_end;       // claimed range (phase selection)
+  const uint32_t* iter;                // device iteration counter (graph mode) or null
   double lr;
   float scale, mu, wd;
   int mode;
@@ -261,6 +261,9 @@ __device__ __forceinline__ void cta_wait_flags(uint32_t* const* flags, int n, ui
 template <int N, class T>
 __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
   constexpr int W = VecT<T>::W;
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
   const int me = a.rank;
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
       uint64_t lo = j * a.sl + (uint64_t)c * a.CH;
       uint64_t hi = min(min(lo + a.CH, (uint64_t)(j + 1) * a.sl), a.S);
       if (lo < hi) {
-        T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * a.sl + (lo - j * a.sl));
+        T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + (lo - j * a.sl));
         uint64_t nvec = (hi - lo + W - 1) / W;
         constexpr int UP = 4;
         for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)UP * blockDim.x) {
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
           for (int u = 0; u < UP; ++u)
             if (cnt[u] > 0) st_vec<T>(dst + (q0 + (uint64_t)u * blockDim.x) * W, cnt[u], buf[u]);
         }
-        cta_release_flag(a.rxflags[j] + (uint64_t)me * a.C + c, a.epoch);
+        cta_release_flag(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
       }
     } else {
       // ---- owner: fold N contributions in tree order, update, all-gather store
@@ -306,8 +309,8 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
         s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)s * a.C + c;
       }
       __syncthreads();
-      cta_wait_flags(s_flags, N - 1, a.epoch, a.st);
-      const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl + (lo - me * a.sl);
+      cta_wait_flags(s_flags, N - 1, epoch, a.st);
+      const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
       uint64_t nvec = (hi - lo + W - 1) / W;
       constexpr int U = N <= 4 ? 2 : 1;
       for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
@@ -330,6 +333,9 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
   constexpr int W = VecT<T>::W;
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
   const int me = a.rank;
@@ -342,8 +348,8 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
     uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
     if (threadIdx.x < (unsigned)nc) s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)threadIdx.x * a.C + c;
     __syncthreads();
-    cta_wait_flags(s_flags, nc, a.epoch, a.st);
-    const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl;
+    cta_wait_flags(s_flags, nc, epoch, a.st);
+    const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl;
     uint64_t nvec = (hi - lo + W - 1) / W;
     for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
       uint64_t e = lo + q * W;
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
         st_vec<T>(wp, cnt, w);
         for (int s = 0; s < nc; ++s) st_vec<T>(static_cast<T*>(a.model[tree_child(0, s)]) + e, cnt, w);
       } else {
-        T* dst = static_cast<T*>(a.rx[parent]) + ((uint64_t)(a.parity * a.K + myslot) * a.sl + e);
+        T* dst = static_cast<T*>(a.rx[parent]) + ((uint64_t)(parity * a.K + myslot) * a.sl + e);
         st_vec<T>(dst, cnt, acc);
       }
     }
@@ -378,12 +384,12 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
       if (threadIdx.x < (unsigned)nc) {
         int child = tree_child(0, threadIdx.x);
         fence_acq_rel_sys();
-        st_release_sys(a.mflags[child] + a.dflag + c, a.epoch);
+        st_release_sys(a.mflags[child] + a.dflag + c, epoch);
         red_release_sys_add(a.mflags[child] + a.layer, 1u);
       }
     } else if (threadIdx.x == 0) {
       fence_acq_rel_sys();
-      st_release_sys(a.rxflags[parent] + (uint64_t)myslot * a.C + c, a.epoch);
+      st_release_sys(a.rxflags[parent] + (uint64_t)myslot * a.C + c, epoch);
     }
   }
   retire(a.queue);
@@ -393,6 +399,7 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
 template <class T>
 __global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
   constexpr int W = VecT<T>::W;
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[1];
   const int me = a.rank;
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
     uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
     if (threadIdx.x == 0) s_flags[0] = a.mflags[me] + a.dflag + c;
     __syncthreads();
-    cta_wait_flags(s_flags, 1, a.epoch, a.st);
+    cta_wait_flags(s_flags, 1, epoch, a.st);
     uint64_t nvec = (hi - lo + W - 1) / W;
     const T* src = static_cast<const T*>(a.model[me]);
     for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
     if (threadIdx.x < (unsigned)nc) {
       int child = tree_child(me, threadIdx.x);
       fence_acq_rel_sys();
-      st_release_sys(a.mflags[child] + a.dflag + c, a.epoch);
+      st_release_sys(a.mflags[child] + a.dflag + c, epoch);
       red_release_sys_add(a.mflags[child] + a.layer, 1u);
     }
   }
@@ -425,8 +432,10 @@ __global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
 }
 
 // Gate: the stream proceeds once `want` chunk arrivals were counted.
-__global__ void k_gate(const uint32_t* counter, uint32_t want, Status st) {
-  if (threadIdx.x == 0) wait_geq(counter, want, st);
+// want = *iter * per_epoch (graph mode: gate for the iteration before the current one)
+__global__ void k_gate(const uint32_t* counter, uint32_t want, const uint32_t* iter, uint32_t add, uint32_t per_epoch,
+                       Status st) {
+  if (threadIdx.x == 0) wait_geq(counter, iter ? (*iter + add) * per_epoch : want, st);
 }
 
 // Copy-engine two-shot (TWOSHOT_CE): the gradient shards and the updated shards
@@ -438,9 +447,24 @@ struct FlagSet {
   const uint32_t* f[PGX_MAX_RANKS];
   int n;
 };
-__global__ void k_wait_flags(FlagSet fs, uint32_t want, Status st) {
-  if (threadIdx.x < (unsigned)fs.n) wait_geq(fs.f[threadIdx.x], want, st);
+__global__ void k_wait_flags(FlagSet fs, uint32_t want, const uint32_t* iter, uint32_t add, Status st) {
+  if (threadIdx.x < (unsigned)fs.n) wait_geq(fs.f[threadIdx.x], iter ? *iter + add : want, st);
 }
+
+// Raise peers' flags after this stream's preceding copies completed (stream order):
+// system fence, then release stores of the epoch.
+struct FlagOut {
+  uint32_t* f[PGX_MAX_RANKS];
+  int n;
+};
+__global__ void k_signal(FlagOut fo, uint32_t value, const uint32_t* iter) {
+  if (threadIdx.x < (unsigned)fo.n) {
+    fence_acq_rel_sys();
+    st_release_sys(fo.f[threadIdx.x], iter ? *iter + 1 : value);
+  }
+}
+
+__global__ void k_tick(uint32_t* iter) { *iter += 1; }
 
 template <int N, class T>
 __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
@@ -494,6 +518,9 @@ struct pgx_xchg {
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
   std::vector<cudaEvent_t> done;
   std::vector<cudaEvent_t> ready;                  // TWOSHOT_CE: gradient ready on the launch stream
+  std::vector<cudaEvent_t> rs_done, down_done;     // side-stream completion (joins for graph capture)
+  uint32_t* iter_dev = nullptr;                    // device iteration counter (graph mode)
+  bool device_iter = false;
   uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
 };
 
@@ -537,6 +564,7 @@ XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
   a.wd = x->cfg.weight_decay;
   a.mode = x->cfg.mode;
   a.st = world_status(x->w);
+  a.iter = x->device_iter ? x->iter_dev : nullptr;
   return a;
 }
 
@@ -579,26 +607,14 @@ void launch_owner_local(int N, int grid, cudaStream_t s, const XArgs& a) {
 
 }  // namespace
 
-// cuStreamWriteValue32 through the runtime's driver entry point, so libpgx.so does
-// not link libcuda (it must load on machines without a driver).
-typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-static WriteValue32Fn write_value32() {
-  static WriteValue32Fn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<WriteValue32Fn>(p);
-  }
-  return fn;
-}
-
-// TWOSHOT_CE launch: reduce-scatter and all-gather as peer DMA copies + fenced
-// stream writes of the notifications; owner fold/update as a local kernel.
+// TWOSHOT_CE launch: reduce-scatter and all-gather as peer DMA copies, each batch
+// followed (in stream order) by k_signal raising the peers' notifications with a
+// system-scope release; owner fold/update as a local kernel.
 static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, cudaStream_t s, int phases) {
   const int N = x->world, me = x->rank;
   const int esz = x->esz;
+  a.parity = 0;  // single-buffered: a sender rewrites a slot only after it gated on this owner's previous
+                 // all-gather, which the owner sends after reading the slot (per-layer forward gate)
   cudaError_t e = cudaEventRecord(x->ready[l], s);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
   if (phases & PGX_PHASE_PUSH) {
@@ -618,12 +634,14 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
         }
         pb = pe;
       }
-      WriteValue32Fn wv = write_value32();
-      if (!wv) return fail(PGX_E_CUDA, "cuStreamWriteValue32 entry point unavailable");
-      CUresult cr = wv((CUstream)x->ce_rs, (CUdeviceptr)(a.rxflags[j] + (uint64_t)me * P.C),
-                                         a.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
-      if (cr != CUDA_SUCCESS) return fail(PGX_E_CUDA, "cuStreamWriteValue32 failed (%d)", (int)cr);
     }
+    FlagOut fo{};
+    for (int d = 1; d < N; ++d) fo.f[fo.n++] = a.rxflags[(me + d) % N] + (uint64_t)me * P.C;
+    if (fo.n) {
+      k_signal<<<1, 32, 0, x->ce_rs>>>(fo, a.epoch, a.iter);
+      ++x->launches;
+    }
+    cudaEventRecord(x->rs_done[l], x->ce_rs);
   }
   if (phases & PGX_PHASE_OWNER) {
     cudaStreamWaitEvent(x->ce_own, x->ready[l], 0);
@@ -632,7 +650,7 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
     for (int sidx = 0; sidx < N; ++sidx)
       if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C;
     if (fs.n) {
-      k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.st);
+      k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
       ++x->launches;
     }
     int grid = std::max(1, std::min(P.grid, (int)((P.sl / VecT<float>::W + kThreads - 1) / kThreads)));
@@ -649,12 +667,13 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
                             (hi - lo) * esz, cudaMemcpyDeviceToDevice, x->ce_own);
         if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
       }
-      WriteValue32Fn wv = write_value32();
-      if (!wv) return fail(PGX_E_CUDA, "cuStreamWriteValue32 entry point unavailable");
-      CUresult cr = wv((CUstream)x->ce_own,
-                                         (CUdeviceptr)(a.mflags[t] + x->ownerflag_base + (uint64_t)l * N + me),
-                                         a.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
-      if (cr != CUDA_SUCCESS) return fail(PGX_E_CUDA, "cuStreamWriteValue32 failed (%d)", (int)cr);
+    }
+    FlagOut fo{};
+    for (int d = 1; d < N; ++d)
+      fo.f[fo.n++] = a.mflags[(me + d) % N] + x->ownerflag_base + (uint64_t)l * N + me;
+    if (fo.n) {
+      k_signal<<<1, 32, 0, x->ce_own>>>(fo, a.epoch, a.iter);
+      ++x->launches;
     }
     e = cudaEventRecord(x->done[l], x->ce_own);
     if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
@@ -775,10 +794,16 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_own, cudaStreamNonBlocking, hi_prio);
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
+    x->rs_done.resize(cfg->num_layers);
+    x->down_done.resize(cfg->num_layers);
     for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l) {
       e = cudaEventCreateWithFlags(&x->done[l], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ready[l], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs_done[l], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->down_done[l], cudaEventDisableTiming);
     }
+    if (e == cudaSuccess) e = cudaMalloc(&x->iter_dev, sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(x->iter_dev, 0xFF, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -800,6 +825,9 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   if (x->queues) cudaFree(x->queues);
   for (auto e : x->done) cudaEventDestroy(e);
   for (auto e : x->ready) cudaEventDestroy(e);
+  for (auto e : x->rs_done) cudaEventDestroy(e);
+  for (auto e : x->down_done) cudaEventDestroy(e);
+  if (x->iter_dev) cudaFree(x->iter_dev);
   if (x->down) cudaStreamDestroy(x->down);
   if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
   if (x->ce_own) cudaStreamDestroy(x->ce_own);
@@ -854,6 +882,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     if (prev != x->dev) cudaSetDevice(prev);
     return rc;
   }
+  cudaEventRecord(x->ready[l], s);
   if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
@@ -887,10 +916,12 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
       // DOWN separately and get the down pass on `stream`)
       cudaStream_t ds = (phases & PGX_PHASE_PUSH) ? x->down : s;
       ++x->launches;
+      if (ds == x->down) cudaStreamWaitEvent(x->down, x->ready[l], 0);
       if (x->esz == 8)
         k_tree_down<double><<<P.down_grid, kThreads, 0, ds>>>(d);
       else
         k_tree_down<float><<<P.down_grid, kThreads, 0, ds>>>(d);
+      cudaEventRecord(x->down_done[l], ds);
     }
   }
   cudaError_t e = cudaGetLastError();
@@ -908,27 +939,51 @@ int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
   cudaError_t e = cudaStreamWaitEvent(s, x->done[l], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, x->rs_done[l], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, x->down_done[l], 0);
+  const uint32_t* it = x->device_iter ? x->iter_dev : nullptr;
   if (e == cudaSuccess && P.variant == PGX_VARIANT_TWOSHOT_CE) {
     FlagSet fs{};
-    for (int j = 0; j < x->world; ++j) {
-      if (j == x->rank) continue;
-      uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
-      (void)lo;
-      (void)hi;
-      fs.f[fs.n++] = x->mflags + x->ownerflag_base + (uint64_t)l * x->world + j;
-    }
+    for (int j = 0; j < x->world; ++j)
+      if (j != x->rank) fs.f[fs.n++] = x->mflags + x->ownerflag_base + (uint64_t)l * x->world + j;
     if (fs.n) {
       ++x->launches;
-      k_wait_flags<<<1, 32, 0, s>>>(fs, iteration + 1, world_status(x->w));
+      k_wait_flags<<<1, 32, 0, s>>>(fs, iteration + 1, it, iteration + 1, world_status(x->w));
       e = cudaGetLastError();
     }
   } else if (e == cudaSuccess && P.expected) {
     ++x->launches;
-    k_gate<<<1, 32, 0, s>>>(x->mflags + l, (iteration + 1) * P.expected, world_status(x->w));
+    k_gate<<<1, 32, 0, s>>>(x->mflags + l, (iteration + 1) * P.expected, it, iteration + 1, P.expected,
+                            world_status(x->w));
     e = cudaGetLastError();
   }
   if (prev != x->dev) cudaSetDevice(prev);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "gate failed: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
+int pgx_xchg_device_iteration(pgx_xchg* x, int enable, uint32_t current) {
+  int prev;
+  cudaGetDevice(&prev);
+  cudaSetDevice(x->dev);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(x->iter_dev, &current, sizeof(uint32_t), cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "device iteration: %s", cudaGetErrorString(e));
+  x->device_iter = enable != 0;
+  return PGX_OK;
+}
+
+int pgx_xchg_tick(pgx_xchg* x, void* stream) {
+  if (!x->device_iter) return fail(PGX_E_CONFIG, "tick needs device-iteration mode");
+  int prev;
+  cudaGetDevice(&prev);
+  if (prev != x->dev) cudaSetDevice(x->dev);
+  k_tick<<<1, 1, 0, (cudaStream_t)stream>>>(x->iter_dev);
+  ++x->launches;
+  cudaError_t e = cudaGetLastError();
+  if (prev != x->dev) cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "tick: %s", cudaGetErrorString(e));
   return PGX_OK;
 }
 
@@ -942,6 +997,8 @@ int pgx_xchg_stream(pgx_xchg* x, int which, void** out) {
 int pgx_xchg_join(pgx_xchg* x, int l, void* stream) {
   if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
   PGX_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, x->done[l], 0));
+  PGX_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, x->rs_done[l], 0));
+  PGX_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, x->down_done[l], 0));
   return PGX_OK;
 }
 

@@ -82,6 +82,7 @@ class DeviceExchange:
         with torch.cuda.device(transport.device):
             self.stream = torch.cuda.Stream(device=transport.device, priority=-1)
         self.connected = False
+        self.device_iteration = False
         self.launches = 0
         self.internal_streams = []
         for which in range(3):
@@ -117,6 +118,16 @@ class DeviceExchange:
         s = (stream or self.stream).cuda_stream
         _lib.call("pgx_xchg_layer", self.handle, layer, iteration & 0xFFFFFFFF, ptrs, cnts, n, phases, s)
         self.launches += 1
+
+    def set_device_iteration(self, enable: bool, current: int) -> None:
+        """Graph mode: epochs come from a device counter (`current` = last launched
+        iteration); capture `tick()` at the start of every step."""
+        _lib.call("pgx_xchg_device_iteration", self.handle, int(bool(enable)), current & 0xFFFFFFFF)
+        self.device_iteration = bool(enable)
+
+    def tick(self, stream=None) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.tr.device)
+        _lib.call("pgx_xchg_tick", self.handle, s.cuda_stream)
 
     def join(self, layer: int, stream) -> None:
         """Make `stream` wait until this rank's part of layer's last exchange is done."""
@@ -174,6 +185,7 @@ class ModuleBinding:
             self._handles.append(mod.register_forward_pre_hook(self._make_gate(l)))
         self.gpu_launches = 0
         self.timed_layers: set = set()   # layers whose launches are bracketed by CUDA events
+        self._tstream = None
         self.events: dict = {}
 
     def _make_hook(self, l):
@@ -190,9 +202,10 @@ class ModuleBinding:
                 g = p.grad
                 if not g.is_contiguous():
                     g = g.contiguous()
-                g.record_stream(self.x.stream)
-                for st in self.x.internal_streams:  # copy-engine variants read it there
-                    g.record_stream(st)
+                if not self.x.device_iteration:  # graph replays keep their pool alive
+                    g.record_stream(self.x.stream)
+                    for st in self.x.internal_streams:  # copy-engine variants read it there
+                        g.record_stream(st)
                 pieces.append(g)
             timed = l in self.timed_layers
             if timed:
@@ -200,8 +213,11 @@ class ModuleBinding:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(self.x.stream)
             self.x.launch(l, self.k, pieces)
-            if timed:
-                e1.record(self.x.stream)
+            if timed:  # end = this rank's part done on every internal stream (copy-engine variants too)
+                if self._tstream is None:
+                    self._tstream = torch.cuda.Stream(device=self.x.tr.device)
+                self.x.join(l, self._tstream)
+                e1.record(self._tstream)
                 self.events.setdefault(l, []).append((e0, e1))
             for p in params:
                 p.grad = None  # next backward allocates fresh gradients; the allocator
@@ -211,7 +227,10 @@ class ModuleBinding:
 
     def _make_gate(self, l):
         def pre_hook(_mod, _inp):
-            if self.k > 0:
+            if self.x.device_iteration:
+                self.x.gate(l, -1)  # relative: the previous iteration
+                self.gpu_launches += 1
+            elif self.k > 0:
                 self.x.gate(l, self.k - 1)
                 self.gpu_launches += 1
         return pre_hook
@@ -220,11 +239,25 @@ class ModuleBinding:
         """Call once per iteration after backward()."""
         self.k += 1
 
+    def begin_step(self) -> None:
+        """Graph mode: advance the device iteration counter (capture this first)."""
+        if self.x.device_iteration:
+            self.x.tick()
+
     def drain(self) -> None:
-        """Gate every layer on the last finished iteration (end of a timed region)."""
-        if self.k > 0:
+        """Gate every layer on the last finished iteration (end of a timed region);
+        in graph mode this also joins the exchange streams back for capture."""
+        if self.x.device_iteration:
+            for l in range(len(self.layers)):
+                self.x.join(l, torch.cuda.current_stream(self.x.tr.device))
+        elif self.k > 0:
             for l in range(len(self.layers)):
                 self.x.gate(l, self.k - 1)
+
+    def wait_current(self) -> None:
+        """Graph mode, outside capture: wait for the latest iteration's weights everywhere."""
+        for l in range(len(self.layers)):
+            self.x.gate(l, 0)
 
     def remove(self) -> None:
         for h in self._handles:

@@ -153,3 +153,62 @@ def test_module_binding_single_gpu_matches_sgd_rule(cuda):
     bind.remove()
     x.close()
     world.close()
+
+
+def _mlp():
+    torch.manual_seed(3)
+    return torch.nn.Sequential(torch.nn.Linear(32, 64), torch.nn.Tanh(), torch.nn.Linear(64, 10)).cuda()
+
+
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce"])
+def test_cuda_graph_replay_matches_eager(cuda, variant):
+    """A captured training step (device iteration counter) gives the same weights as eager steps."""
+    from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
+    from paper_1706_00095_b200.transport import LocalWorld
+
+    data = torch.randn(16, 32, device="cuda")
+    results = []
+    for graph_mode in (False, True):
+        net = _mlp()
+        layers = [(net[0], [net[0].weight, net[0].bias]), (net[2], [net[2].weight, net[2].bias])]
+        world = LocalWorld(1, inline=False)
+        tr = world.transport(0)
+        x = DeviceExchange(tr, [sum(p.numel() for p in ps) for _, ps in layers], mode="fast32", variant=variant,
+                           lr=0.05, momentum=0.9, weight_decay=1e-3)
+        x.connect()
+        bind = ModuleBinding(x, layers)
+
+        def step():
+            loss = net(data).square().mean()
+            loss.backward()
+            bind.step_done()
+            return loss
+
+        for _ in range(2):  # eager warm-up, host iterations 0, 1
+            step()
+        bind.drain()
+        torch.cuda.synchronize()
+        if graph_mode:
+            x.set_device_iteration(True, bind.k - 1)
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
+                bind.begin_step()
+                step()
+                bind.drain()
+            torch.cuda.current_stream().wait_stream(cap)
+            for _ in range(4):
+                g.replay()
+            bind.wait_current()
+        else:
+            for _ in range(4):
+                step()
+            bind.drain()
+        torch.cuda.synchronize()
+        assert tr.device_status() == 0
+        results.append(x.model.clone().cpu())
+        bind.remove()
+        x.close()
+        world.close()
+    assert torch.equal(results[0], results[1])
