@@ -496,6 +496,31 @@ struct LayerPlan {
 
 }  // namespace
 
+// An event plus where it was last recorded: eagerly (cap = 0) or inside the stream
+// capture with id `cap`.  Waits only bind to records of the same capture (or eager
+// records from eager streams) — a captured graph may not depend on uncaptured work.
+struct XEvent {
+  cudaEvent_t e = nullptr;
+  unsigned long long cap = 0;
+  bool valid = false;
+};
+
+static unsigned long long capture_id(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  unsigned long long id = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, &id) != cudaSuccess) return 0;
+  return st == cudaStreamCaptureStatusActive ? id : 0;
+}
+static cudaError_t xrecord(XEvent& ev, cudaStream_t s) {
+  ev.cap = capture_id(s);
+  ev.valid = true;
+  return cudaEventRecord(ev.e, s);
+}
+static cudaError_t xwait(cudaStream_t s, const XEvent& ev) {
+  if (!ev.valid || ev.cap != capture_id(s)) return cudaSuccess;
+  return cudaStreamWaitEvent(s, ev.e, 0);
+}
+
 struct pgx_xchg {
   pgx_world* w = nullptr;
   pgx_xchg_config cfg{};
@@ -516,9 +541,9 @@ struct pgx_xchg {
   uint64_t launches = 0;
   cudaStream_t down = nullptr;
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
-  std::vector<cudaEvent_t> done;
-  std::vector<cudaEvent_t> ready;                  // TWOSHOT_CE: gradient ready on the launch stream
-  std::vector<cudaEvent_t> rs_done, down_done;     // side-stream completion (joins for graph capture)
+  std::vector<XEvent> done;
+  std::vector<XEvent> ready;                       // gradient ready on the launch stream
+  std::vector<XEvent> rs_done, down_done;          // side-stream completion (joins for graph capture)
   uint32_t* iter_dev = nullptr;                    // device iteration counter (graph mode)
   bool device_iter = false;
   uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
@@ -615,10 +640,10 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
   const int esz = x->esz;
   a.parity = 0;  // single-buffered: a sender rewrites a slot only after it gated on this owner's previous
                  // all-gather, which the owner sends after reading the slot (per-layer forward gate)
-  cudaError_t e = cudaEventRecord(x->ready[l], s);
+  cudaError_t e = xrecord(x->ready[l], s);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
   if (phases & PGX_PHASE_PUSH) {
-    cudaStreamWaitEvent(x->ce_rs, x->ready[l], 0);
+    xwait(x->ce_rs, x->ready[l]);
     for (int d = 1; d < N; ++d) {
       int j = (me + d) % N;
       uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
@@ -641,10 +666,10 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
       k_signal<<<1, 32, 0, x->ce_rs>>>(fo, a.epoch, a.iter);
       ++x->launches;
     }
-    cudaEventRecord(x->rs_done[l], x->ce_rs);
+    xrecord(x->rs_done[l], x->ce_rs);
   }
   if (phases & PGX_PHASE_OWNER) {
-    cudaStreamWaitEvent(x->ce_own, x->ready[l], 0);
+    xwait(x->ce_own, x->ready[l]);
     FlagSet fs{};
     fs.n = 0;
     for (int sidx = 0; sidx < N; ++sidx)
@@ -675,7 +700,7 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
       k_signal<<<1, 32, 0, x->ce_own>>>(fo, a.epoch, a.iter);
       ++x->launches;
     }
-    e = cudaEventRecord(x->done[l], x->ce_own);
+    e = xrecord(x->done[l], x->ce_own);
     if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
   }
   return PGX_OK;
@@ -797,10 +822,10 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     x->rs_done.resize(cfg->num_layers);
     x->down_done.resize(cfg->num_layers);
     for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l) {
-      e = cudaEventCreateWithFlags(&x->done[l], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ready[l], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs_done[l], cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->down_done[l], cudaEventDisableTiming);
+      e = cudaEventCreateWithFlags(&x->done[l].e, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ready[l].e, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs_done[l].e, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->down_done[l].e, cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaMalloc(&x->iter_dev, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(x->iter_dev, 0xFF, sizeof(uint32_t));
@@ -823,10 +848,10 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   cudaDeviceSynchronize();
   if (x->v) cudaFree(x->v);
   if (x->queues) cudaFree(x->queues);
-  for (auto e : x->done) cudaEventDestroy(e);
-  for (auto e : x->ready) cudaEventDestroy(e);
-  for (auto e : x->rs_done) cudaEventDestroy(e);
-  for (auto e : x->down_done) cudaEventDestroy(e);
+  for (auto& e : x->done) cudaEventDestroy(e.e);
+  for (auto& e : x->ready) cudaEventDestroy(e.e);
+  for (auto& e : x->rs_done) cudaEventDestroy(e.e);
+  for (auto& e : x->down_done) cudaEventDestroy(e.e);
   if (x->iter_dev) cudaFree(x->iter_dev);
   if (x->down) cudaStreamDestroy(x->down);
   if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
@@ -882,7 +907,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     if (prev != x->dev) cudaSetDevice(prev);
     return rc;
   }
-  cudaEventRecord(x->ready[l], s);
+  xrecord(x->ready[l], s);
   if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
@@ -916,16 +941,16 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
       // DOWN separately and get the down pass on `stream`)
       cudaStream_t ds = (phases & PGX_PHASE_PUSH) ? x->down : s;
       ++x->launches;
-      if (ds == x->down) cudaStreamWaitEvent(x->down, x->ready[l], 0);
+      if (ds == x->down) xwait(x->down, x->ready[l]);
       if (x->esz == 8)
         k_tree_down<double><<<P.down_grid, kThreads, 0, ds>>>(d);
       else
         k_tree_down<float><<<P.down_grid, kThreads, 0, ds>>>(d);
-      cudaEventRecord(x->down_done[l], ds);
+      xrecord(x->down_done[l], ds);
     }
   }
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaEventRecord(x->done[l], s);
+  if (e == cudaSuccess) e = xrecord(x->done[l], s);
   if (prev != x->dev) cudaSetDevice(prev);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "exchange launch failed: %s", cudaGetErrorString(e));
   return PGX_OK;
@@ -938,9 +963,9 @@ int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
   int prev;
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
-  cudaError_t e = cudaStreamWaitEvent(s, x->done[l], 0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, x->rs_done[l], 0);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, x->down_done[l], 0);
+  cudaError_t e = xwait(s, x->done[l]);
+  if (e == cudaSuccess) e = xwait(s, x->rs_done[l]);
+  if (e == cudaSuccess) e = xwait(s, x->down_done[l]);
   const uint32_t* it = x->device_iter ? x->iter_dev : nullptr;
   if (e == cudaSuccess && P.variant == PGX_VARIANT_TWOSHOT_CE) {
     FlagSet fs{};
@@ -996,9 +1021,9 @@ int pgx_xchg_stream(pgx_xchg* x, int which, void** out) {
 
 int pgx_xchg_join(pgx_xchg* x, int l, void* stream) {
   if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
-  PGX_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, x->done[l], 0));
-  PGX_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, x->rs_done[l], 0));
-  PGX_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, x->down_done[l], 0));
+  PGX_CUDA(xwait((cudaStream_t)stream, x->done[l]));
+  PGX_CUDA(xwait((cudaStream_t)stream, x->rs_done[l]));
+  PGX_CUDA(xwait((cudaStream_t)stream, x->down_done[l]));
   return PGX_OK;
 }
 

@@ -133,3 +133,124 @@ def test_host_engine_over_ipc_matches_sequential(pattern):
     for rank, ok, barriers in out:
         assert ok is True, (rank, ok)
         assert barriers == (0 if pattern == "pipelined" else 8)
+
+
+def _lenet():
+    import torch.nn as nn
+
+    class LeNet(nn.Module):  # Caffe lenet_train_test.prototxt: 520 / 25,050 / 400,500 / 5,010 params
+        def __init__(self):
+            super().__init__()
+            self.conv1 = nn.Conv2d(1, 20, 5)
+            self.conv2 = nn.Conv2d(20, 50, 5)
+            self.ip1 = nn.Linear(800, 500)
+            self.ip2 = nn.Linear(500, 10)
+
+        def forward(self, x):
+            x = torch.max_pool2d(self.conv1(x), 2, 2)
+            x = torch.max_pool2d(self.conv2(x), 2, 2)
+            return self.ip2(torch.relu(self.ip1(x.flatten(1))))
+
+        def layers(self):
+            return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.ip1, self.ip2)]
+
+    return LeNet()
+
+
+def _cifar10_quick():
+    import torch.nn as nn
+
+    class Quick(nn.Module):  # Caffe cifar10_quick: 2,432 / 25,632 / 51,264 / 65,600 / 650 params
+        def __init__(self):
+            super().__init__()
+            self.conv1 = nn.Conv2d(3, 32, 5, padding=2)
+            self.conv2 = nn.Conv2d(32, 32, 5, padding=2)
+            self.conv3 = nn.Conv2d(32, 64, 5, padding=2)
+            self.ip1 = nn.Linear(1024, 64)
+            self.ip2 = nn.Linear(64, 10)
+
+        def forward(self, x):
+            x = torch.relu(torch.max_pool2d(self.conv1(x), 3, 2, ceil_mode=True))
+            x = torch.avg_pool2d(torch.relu(self.conv2(x)), 3, 2, ceil_mode=True)
+            x = torch.avg_pool2d(torch.relu(self.conv3(x)), 3, 2, ceil_mode=True)
+            return self.ip2(self.ip1(x.flatten(1)))
+
+        def layers(self):
+            return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.conv3, self.ip1, self.ip2)]
+
+    return Quick()
+
+
+def _model_worker(rank, world, port, which, variant, q):
+    """configs[0] / configs[1]: a real model trained through ModuleBinding; every step's
+    exchanged weights must equal the oracle applied to the gradients the hooks saw."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    from oracle import pipesgd_oracle as O
+    from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
+    from paper_1706_00095_b200.transport import DistTransport
+
+    try:
+        torch.manual_seed(0)  # identical init on every rank
+        net = (_lenet() if which == "lenet" else _cifar10_quick()).cuda()
+        layers = net.layers()
+        if which == "lenet":
+            shape, batch, hyper = (1, 28, 28), 64 // world, dict(lr=0.01, momentum=0.0, weight_decay=0.0)
+        else:
+            shape, batch, hyper = (3, 32, 32), 100, dict(lr=0.001, momentum=0.9, weight_decay=0.004)
+        tr = DistTransport(rank, world, rank, timeout_s=20.0)
+        x = DeviceExchange(tr, [sum(p.numel() for p in ps) for _, ps in layers], mode="fast32", variant=variant,
+                           **hyper)
+        bind = ModuleBinding(x, layers)
+        tr.barrier()
+        x.connect()
+        seen = {}
+        orig = x.launch
+
+        def spy(layer, iteration, pieces, stream=None, phases=7):
+            seen[layer] = torch.cat([p.detach().reshape(-1) for p in pieces]).clone()
+            return orig(layer, iteration, pieces, stream, phases)
+
+        x.launch = spy
+        g = torch.Generator(device="cpu").manual_seed(42 + rank)
+        w = [x.layer_views[l].cpu().numpy().copy() for l in range(len(layers))]
+        v = [np.zeros_like(a) for a in w]
+        bad = []
+        for k in range(3):
+            data = torch.randn(batch, *shape, generator=g).cuda()
+            label = torch.randint(0, 10, (batch,), generator=g).cuda()
+            loss = torch.nn.functional.cross_entropy(net(data), label)
+            loss.backward()
+            bind.step_done()
+            bind.drain()
+            torch.cuda.synchronize()
+            for l in range(len(layers)):
+                every = [None] * world
+                dist.all_gather_object(every, seen[l].cpu().numpy())
+                w[l], v[l] = O.exchange_iteration(every, w[l], hyper["lr"], "fast32", state=v[l],
+                                                  scale=1.0 / world, momentum=hyper["momentum"],
+                                                  weight_decay=hyper["weight_decay"])
+                got = x.layer_views[l].cpu().numpy()
+                if got.tobytes() != w[l].tobytes():
+                    bad.append((k, l, float(np.max(np.abs(got - w[l])))))
+        q.put((rank, bad, tr.device_status()))
+        x.close()
+        tr.close()
+    except Exception as exc:  # noqa: BLE001
+        import traceback
+
+        q.put((rank, traceback.format_exc(), -1))
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("which", ["lenet", "cifar10_quick"])
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "tree"])
+def test_real_models_match_oracle(which, variant):
+    world = 2 if which == "lenet" else min(4, _ngpu())
+    out = _spawn(_model_worker, world, which, variant)
+    for rank, bad, status in out:
+        assert bad == [] and status == 0, (rank, bad, status)
