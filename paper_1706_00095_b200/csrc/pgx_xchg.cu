@@ -502,6 +502,7 @@ struct LayerPlan {
 struct XEvent {
   cudaEvent_t e = nullptr;
   unsigned long long cap = 0;
+  cudaStream_t rec = nullptr;
   bool valid = false;
 };
 
@@ -513,12 +514,17 @@ static unsigned long long capture_id(cudaStream_t s) {
 }
 static cudaError_t xrecord(XEvent& ev, cudaStream_t s) {
   ev.cap = capture_id(s);
+  ev.rec = s;
   ev.valid = true;
   return cudaEventRecord(ev.e, s);
 }
+// Wait when both sides are eager, when both belong to the same capture, or to fork an
+// eager stream into a live capture (the event was recorded by a stream still capturing).
 static cudaError_t xwait(cudaStream_t s, const XEvent& ev) {
-  if (!ev.valid || ev.cap != capture_id(s)) return cudaSuccess;
-  return cudaStreamWaitEvent(s, ev.e, 0);
+  if (!ev.valid) return cudaSuccess;
+  const unsigned long long c = capture_id(s);
+  bool wait = ev.cap == 0 ? c == 0 : (c == ev.cap || (c == 0 && capture_id(ev.rec) == ev.cap));
+  return wait ? cudaStreamWaitEvent(s, ev.e, 0) : cudaSuccess;
 }
 
 struct pgx_xchg {

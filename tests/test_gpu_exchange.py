@@ -155,60 +155,64 @@ def test_module_binding_single_gpu_matches_sgd_rule(cuda):
     world.close()
 
 
-def _mlp():
-    torch.manual_seed(3)
-    return torch.nn.Sequential(torch.nn.Linear(32, 64), torch.nn.Tanh(), torch.nn.Linear(64, 10)).cuda()
+class _FixedGrad(torch.nn.Module):
+    """loss = sum(w * c) + sum(b * d): its gradient is exactly (c, d) every step (no GEMM
+    rounding), so graph replays and eager steps must both equal the oracle bit for bit."""
+
+    def __init__(self, n, seed):
+        super().__init__()
+        gen = torch.Generator().manual_seed(seed)
+        self.weight = torch.nn.Parameter(torch.randn(n, generator=gen).cuda())
+        self.bias = torch.nn.Parameter(torch.randn(7, generator=gen).cuda())
+        self.c = (torch.randn(n, generator=gen) * 1e-2).cuda()
+        self.d = (torch.randn(7, generator=gen) * 1e-2).cuda()
+
+    def forward(self):
+        return (self.weight * self.c).sum() + (self.bias * self.d).sum()
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce"])
-def test_cuda_graph_replay_matches_eager(cuda, variant):
-    """A captured training step (device iteration counter) gives the same weights as eager steps."""
+def test_cuda_graph_replay_matches_oracle(cuda, variant):
+    """A captured training step (device iteration counter) applies exactly the oracle update."""
     from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
     from paper_1706_00095_b200.transport import LocalWorld
 
-    data = torch.randn(16, 32, device="cuda")
-    results = []
-    for graph_mode in (False, True):
-        net = _mlp()
-        layers = [(net[0], [net[0].weight, net[0].bias]), (net[2], [net[2].weight, net[2].bias])]
-        world = LocalWorld(1, inline=False)
-        tr = world.transport(0)
-        x = DeviceExchange(tr, [sum(p.numel() for p in ps) for _, ps in layers], mode="fast32", variant=variant,
-                           lr=0.05, momentum=0.9, weight_decay=1e-3)
-        x.connect()
-        bind = ModuleBinding(x, layers)
+    m = _FixedGrad(40000, 5)
+    layers = [(m, [m.weight, m.bias])]
+    world = LocalWorld(1, inline=False)
+    tr = world.transport(0)
+    x = DeviceExchange(tr, [40007], mode="fast32", variant=variant, lr=0.05, momentum=0.9, weight_decay=1e-3)
+    x.connect()
+    w = torch.cat([m.weight.detach(), m.bias.detach()]).cpu().numpy()
+    g = torch.cat([m.c, m.d]).cpu().numpy()
+    bind = ModuleBinding(x, layers)
+    v = np.zeros_like(w)
 
-        def step():
-            loss = net(data).square().mean()
-            loss.backward()
-            bind.step_done()
-            return loss
+    def step():
+        m().backward()
+        bind.step_done()
 
-        for _ in range(2):  # eager warm-up, host iterations 0, 1
-            step()
+    for _ in range(2):
+        step()
+    bind.drain()
+    torch.cuda.synchronize()
+    x.set_device_iteration(True, bind.k - 1)
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap), torch.cuda.graph(graph, stream=cap):
+        bind.begin_step()
+        step()
         bind.drain()
-        torch.cuda.synchronize()
-        if graph_mode:
-            x.set_device_iteration(True, bind.k - 1)
-            g = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream()
-            cap.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
-                bind.begin_step()
-                step()
-                bind.drain()
-            torch.cuda.current_stream().wait_stream(cap)
-            for _ in range(4):
-                g.replay()
-            bind.wait_current()
-        else:
-            for _ in range(4):
-                step()
-            bind.drain()
-        torch.cuda.synchronize()
-        assert tr.device_status() == 0
-        results.append(x.model.clone().cpu())
-        bind.remove()
-        x.close()
-        world.close()
-    assert torch.equal(results[0], results[1])
+    torch.cuda.current_stream().wait_stream(cap)
+    for _ in range(4):
+        graph.replay()
+    bind.wait_current()
+    torch.cuda.synchronize()
+    for _ in range(6):
+        w, v = O.fast32_update(w, v, g, 1.0, 0.05, 0.9, 1e-3)
+    assert tr.device_status() == 0
+    assert x.layer_views[0].cpu().numpy().tobytes() == w.tobytes()
+    bind.remove()
+    x.close()
+    world.close()
