@@ -26,15 +26,26 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-GLOBAL_BATCH = 256
+GLOBAL_BATCH = 256  # AlexNet, BASELINE.json configs[2]
 ALEXNET_LAYERS = [34944, 307456, 885120, 663936, 442624, 37752832, 16781312, 4097000]
 METRIC = "AlexNet images/sec (B=256 global, synthetic 227x227), per-layer gradient exchange"
+
+
+def wl_of(args):
+    from workloads import WORKLOADS
+
+    return WORKLOADS[args.workload]
+
+
+def global_batch(wl, world):
+    return wl["global_batch"] if "global_batch" in wl else wl["per_gpu_batch"] * world
 NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (900 nominal)
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--workload", default="alexnet", choices=["alexnet", "googlenet"])
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
@@ -64,14 +75,13 @@ CPU_SAMPLE_IMAGES = 8
 
 
 def _cpu_fwd_bwd(model, x, y):
-    import torch
-
-    loss = torch.nn.functional.cross_entropy(model(x), y)
+    loss = model.loss(model(x), y)
     loss.backward()
     model.zero_grad(set_to_none=True)
 
 
-def cpu_step_timing(world: int, *, steps: int | None = None, seconds: float | None = None, warmup: int = 1):
+def cpu_step_timing(world: int, *, steps: int | None = None, seconds: float | None = None, warmup: int = 1,
+                    workload: str = "alexnet"):
     """The same training step on the host CPU: AlexNet forward+backward in PyTorch-CPU
     fp32 on a bounded sample of CPU_SAMPLE_IMAGES images (per-image cost scaled to the
     256-image global batch), plus the reference's exchange data plane (tree fold, master
@@ -83,11 +93,16 @@ def cpu_step_timing(world: int, *, steps: int | None = None, seconds: float | No
 
     model_name, ncpu = cpu_info()
     torch.set_num_threads(ncpu)
-    net = alexnet()
+    from workloads import WORKLOADS
+
+    wl = WORKLOADS[workload]
+    net = wl["cls"]()
+    gb = global_batch(wl, world)
+    sizes = [sum(p.numel() for p in ps) for _, ps in net.layers()]
     g = torch.Generator().manual_seed(0)
-    x = torch.randn(CPU_SAMPLE_IMAGES, 3, 227, 227, generator=g)
+    x = torch.randn(CPU_SAMPLE_IMAGES, 3, wl["image"], wl["image"], generator=g)
     y = torch.randint(0, 1000, (CPU_SAMPLE_IMAGES,), generator=g)
-    ex = CO.ExchangeWorld(world, ALEXNET_LAYERS)
+    ex = CO.ExchangeWorld(world, sizes)
     for _ in range(warmup):
         _cpu_fwd_bwd(net, x, y)
         ex.iteration("fast32", threads=ncpu)
@@ -99,17 +114,17 @@ def cpu_step_timing(world: int, *, steps: int | None = None, seconds: float | No
         t1 = time.perf_counter()
         ex.iteration("fast32", lr=0.01, mu=0.9, wd=5e-4, threads=ncpu)
         t2 = time.perf_counter()
-        fb.append((t1 - t0) * GLOBAL_BATCH / CPU_SAMPLE_IMAGES)
+        fb.append((t1 - t0) * gb / CPU_SAMPLE_IMAGES)
         xc.append(t2 - t1)
     t_fb, t_x = statistics.median(fb), statistics.median(xc)
     t = t_fb + t_x
-    return {"value": GLOBAL_BATCH / t, "unit": "images/s", "cores": ncpu, "kind": "port",
-            "sample": f"{len(fb)} steps; each: AlexNet fwd+bwd of {CPU_SAMPLE_IMAGES} images in PyTorch-CPU fp32 "
-                      f"scaled x{GLOBAL_BATCH // CPU_SAMPLE_IMAGES} to the 256-image batch, plus one full "
-                      f"exchange of the 60,965,224 fp32 params at world {world} (C port of the reference's tree "
+    return {"value": gb / t, "unit": "images/s", "cores": ncpu, "kind": "port",
+            "sample": f"{len(fb)} steps; each: {workload} fwd+bwd of {CPU_SAMPLE_IMAGES} images in PyTorch-CPU fp32 "
+                      f"scaled x{gb / CPU_SAMPLE_IMAGES:g} to the {gb}-image step, plus one full "
+                      f"exchange of the {sum(sizes):,} fp32 params at world {world} (C port of the reference's tree "
                       f"fold + update + broadcast); cpu {model_name}",
             "ms_per_step": t * 1e3, "ms_fwd_bwd": t_fb * 1e3, "ms_exchange": t_x * 1e3,
-            "exchange_only_images_per_s": GLOBAL_BATCH / t_x}
+            "exchange_only_images_per_s": gb / t_x}
 
 
 def reference_arm(args):
@@ -117,10 +132,10 @@ def reference_arm(args):
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    r = cpu_step_timing(world, steps=args.steps, warmup=max(1, min(args.warmup, 2)))
-    line = {"metric": METRIC, "value": r["value"], "unit": "images/s", "n_gpus": world, "steps": args.steps,
+    r = cpu_step_timing(world, steps=args.steps, warmup=max(1, min(args.warmup, 2)), workload=args.workload)
+    line = {"metric": wl_of(args)["metric"], "value": r["value"], "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "scaling": wl_of(args)["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": workload_config(world, args),
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "ms_fwd_bwd",
                                                "ms_exchange", "exchange_only_images_per_s")},
@@ -129,48 +144,23 @@ def reference_arm(args):
 
 
 def workload_config(world, args):
-    return {"workload": "alexnet_b256_synthetic_227", "model": "AlexNet (BVLC, grouped conv, LRN)",
-            "global_batch": GLOBAL_BATCH, "per_gpu_batch": GLOBAL_BATCH // world, "image": [3, 227, 227],
-            "parallelism": f"dp{world}", "exchange": args.variant, "update": "fast32 momentum SGD lr 0.01 mu 0.9 "
-            "wd 5e-4 scale 1/N", "fwd_bwd": "PyTorch cuDNN bf16 autocast, fp32 master weights/grads",
+    wl = wl_of(args)
+    gb = global_batch(wl, world)
+    name = {"alexnet": "alexnet_b256_synthetic_227", "googlenet": "googlenet_b32pergpu_synthetic_224"}[args.workload]
+    model = {"alexnet": "AlexNet (BVLC, grouped conv, LRN)",
+             "googlenet": "GoogLeNet (BVLC, both aux heads, 64 param layers)"}[args.workload]
+    h = wl["hyper"]
+    return {"workload": name, "model": model,
+            "global_batch": gb, "per_gpu_batch": gb // world, "image": [3, wl["image"], wl["image"]],
+            "parallelism": f"dp{world}", "exchange": args.variant, "update": f"fast32 momentum SGD lr {h['lr']} mu {h['momentum']} "
+            f"wd {h['weight_decay']} scale 1/N", "fwd_bwd": "PyTorch cuDNN bf16 autocast, fp32 master weights/grads",
             "l2": "working set > L2 (244 MB fp32 weights + 244 MB grads + activations per step)",
             "chunk_elems": args.chunk_elems, "step": "CUDA graph replay" if not args.no_graph else "eager"}
 
 
 # ------------------------------------------------------------------ model
 def alexnet():
-    import torch.nn as nn
-
-    class AlexNet(nn.Module):
-        def __init__(self):
-            super().__init__()
-            self.conv1 = nn.Conv2d(3, 96, 11, stride=4)
-            self.conv2 = nn.Conv2d(96, 256, 5, padding=2, groups=2)
-            self.conv3 = nn.Conv2d(256, 384, 3, padding=1)
-            self.conv4 = nn.Conv2d(384, 384, 3, padding=1, groups=2)
-            self.conv5 = nn.Conv2d(384, 256, 3, padding=1, groups=2)
-            self.fc6 = nn.Linear(9216, 4096)
-            self.fc7 = nn.Linear(4096, 4096)
-            self.fc8 = nn.Linear(4096, 1000)
-            self.relu = nn.ReLU(inplace=True)
-            self.lrn = nn.LocalResponseNorm(5, alpha=1e-4, beta=0.75)
-            self.pool = nn.MaxPool2d(3, 2)
-            self.drop = nn.Dropout(0.5)
-
-        def forward(self, x):
-            x = self.pool(self.lrn(self.relu(self.conv1(x))))
-            x = self.pool(self.lrn(self.relu(self.conv2(x))))
-            x = self.relu(self.conv3(x))
-            x = self.relu(self.conv4(x))
-            x = self.pool(self.relu(self.conv5(x)))
-            x = x.flatten(1)
-            x = self.drop(self.relu(self.fc6(x)))
-            x = self.drop(self.relu(self.fc7(x)))
-            return self.fc8(x)
-
-        def layers(self):
-            return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.conv3, self.conv4, self.conv5,
-                                                     self.fc6, self.fc7, self.fc8)]
+    from workloads import AlexNet
 
     return AlexNet()
 
@@ -246,10 +236,12 @@ def pgx_arm(args):
     torch.backends.cudnn.benchmark = True
     torch.manual_seed(1234 + rank)
 
-    model = alexnet().to(dev)
+    wl = wl_of(args)
+    model = wl["cls"]().to(dev)
+    sizes = [sum(p.numel() for p in ps) for _, ps in model.layers()]
     tr = DistTransport(rank, world, local, timeout_s=60.0)
-    xchg = DeviceExchange(tr, ALEXNET_LAYERS, mode="fast32", variant=args.variant, chunk_elems=args.chunk_elems,
-                          lr=0.01, momentum=0.9, weight_decay=5e-4, scale=1.0 / world, max_ctas=args.max_ctas)
+    xchg = DeviceExchange(tr, sizes, mode="fast32", variant=args.variant, chunk_elems=args.chunk_elems,
+                          scale=1.0 / world, max_ctas=args.max_ctas, **wl["hyper"])
     bind = ModuleBinding(xchg, model.layers())
     if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)
         flat = xchg.model.cpu()
@@ -259,20 +251,20 @@ def pgx_arm(args):
     tr.barrier()      # rendezvous: every rank's segments attached over CUDA IPC
     xchg.connect()
 
-    B = args.per_gpu_batch or GLOBAL_BATCH // world
+    B = args.per_gpu_batch or global_batch(wl, world) // world
+    IMG = wl["image"]
     gb = B * world  # images per step, whole job
     g = torch.Generator().manual_seed(42 + rank)
-    host_x = torch.randint(0, 256, (B, 3, 227, 227), dtype=torch.uint8, generator=g).pin_memory()
+    host_x = torch.randint(0, 256, (B, 3, IMG, IMG), dtype=torch.uint8, generator=g).pin_memory()
     host_y = torch.randint(0, 1000, (B,), dtype=torch.int64, generator=g).pin_memory()
     dev_x, dev_y = host_x.to(dev), host_y.to(dev)
     loss_host = torch.zeros(max(args.steps, 1), dtype=torch.float32).pin_memory()
-    crit = torch.nn.CrossEntropyLoss()
 
     def step(xb, yb):
         xin = xb.to(torch.bfloat16, memory_format=torch.channels_last).sub_(128.0).mul_(1.0 / 64.0)
         with torch.autocast("cuda", dtype=torch.bfloat16):
             out = model(xin)
-        loss = crit(out.float(), yb)
+        loss = model.loss(out, yb)
         loss.backward()
         bind.step_done()
         return loss
@@ -304,10 +296,12 @@ def pgx_arm(args):
         step(dev_x, dev_y)
     bind.drain()
     torch.cuda.synchronize()
-    L_DOM = 5  # fc6: the dominant exchange/update kernel (37.75M params)
+    L_DOM = max(range(len(sizes)), key=lambda l: sizes[l])  # the dominant (largest) layer; AlexNet: fc6
 
     # ---- capture one training step as a CUDA graph (epochs from the device counter) ----
     graph = None
+    bind.timed_layers = {L_DOM}  # bracket the dominant layer's exchange with (external) events
+    bind.events.clear()
     if not args.no_graph:
         k_before_capture = bind.k
         xchg.set_device_iteration(True, bind.k - 1)
@@ -384,19 +378,25 @@ def pgx_arm(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * world, "ms_per_step": ms_e2e / args.steps,
                "final_loss": float(loss_host[(args.steps - 1) % loss_host.numel()])}
 
-    # ---- roofline pass: the same steps run eagerly with the fc6 launch bracketed by events ----
+    # ---- dominant-layer exchange time inside steps: the events captured in the graph (or
+    # recorded by every eager step) bracket that layer's exchange on its streams ----
+    durs = []
     if graph is not None:
+        for _ in range(5):  # a few more replays, each read back (the captured events hold the last one)
+            run_step()
+            torch.cuda.synchronize()
+            a, b_ = bind.events[L_DOM][0]
+            durs.append(a.elapsed_time(b_))
+        bind.wait_current()
         torch.cuda.synchronize()
-        bind.k = k_before_capture + replays[0]  # continue the epoch sequence after the replays
+        bind.k = k_before_capture + replays[0]  # continue the epoch sequence eagerly after the replays
         xchg.set_device_iteration(False, 0)
-    bind.timed_layers = {L_DOM}
-    bind.events.clear()
-    ms_eager = timed(lambda i: step(dev_x, dev_y), args.steps)
-    durs = [a.elapsed_time(b) for a, b in bind.events.get(L_DOM, [])]
+    else:
+        durs = [a.elapsed_time(b_) for a, b_ in bind.events.get(L_DOM, [])]
     bind.timed_layers = set()
 
     # ---- dominant kernel in isolation (same launch, no concurrent backward) ----
-    gfc6 = [torch.randn(4096, 9216, device=dev) * 1e-3, torch.randn(4096, device=dev) * 1e-3]
+    gfc6 = [torch.randn_like(p) * 1e-3 for p in model.layers()[L_DOM][1]]
     iso = []
     if world == 1:
         for i in range(10):
@@ -415,23 +415,23 @@ def pgx_arm(args):
     if avg:
         ach = hbm / (avg / 1e3) / 1e9
         peak, peak_src = hbm_peak()
-        roof = {"bound": "hbm", "kernel": "k_twoshot (fc6 fold + fused momentum update%s)" %
-                (" + RS/AG peer stores" if world > 1 else ""), "achieved": ach, "peak": peak, "unit": "GB/s",
+        kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local", "tree": "k_tree_up"}.get(args.variant, "")
+        roof = {"bound": "hbm", "kernel": "%s (layer %d, %d params: fold + fused momentum update%s)" %
+                (kname, L_DOM, sizes[L_DOM], " + peer transfers" if world > 1 else ""), "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": None, "algorithmic_bytes_per_launch": hbm,
                 "avg_launch_ms_in_step": avg, "peak_source": peak_src,
-                "launch_share_of_step": avg / (ms_eager / args.steps),
-                "measured_in": "eager timed region of %d steps (%.3f ms/step) right after the graph-replay region"
-                % (args.steps, ms_eager / args.steps)}
+                "launch_share_of_step": avg / (ms / args.steps),
+                "measured_in": ("CUDA events captured in the step graph, %d replays after the timed region"
+                                % len(durs)) if graph is not None else "CUDA events in every timed eager step"}
         if iso:
             roof["isolated_launch_ms"] = statistics.median(iso)
             roof["isolated_achieved"] = hbm / (statistics.median(iso) / 1e3) / 1e9
             roof["isolated_frac"] = roof["isolated_achieved"] / peak
-    line = {"metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+    line = {"metric": wl["metric"], "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
-            "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None,
-            "ms_per_step_eager": ms_eager / args.steps}
+            "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None}
     if args.per_gpu_batch:
         line["config"]["per_gpu_batch"] = B
         line["config"]["global_batch"] = gb
@@ -441,7 +441,7 @@ def pgx_arm(args):
                                    "unit": "GB/s", "frac": nvl / (avg / 1e3) / 1e9 / NVLINK_PEAK_GBS,
                                    "bytes_per_launch": nvl, "peak_source": "B200_PROFILING.md measured peer copy"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_step_timing(world, seconds=args.cpu_seconds)
+        line["cpu_baseline"] = cpu_step_timing(world, seconds=args.cpu_seconds, workload=args.workload)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if tr.device_status() != 0:

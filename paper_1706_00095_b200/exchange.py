@@ -208,9 +208,10 @@ class ModuleBinding:
                         g.record_stream(st)
                 pieces.append(g)
             timed = l in self.timed_layers
-            if timed:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
+            if timed:  # external events become event-record nodes when captured in a graph
+                ext = torch.cuda.is_current_stream_capturing()
+                e0 = torch.cuda.Event(enable_timing=True, external=ext)
+                e1 = torch.cuda.Event(enable_timing=True, external=ext)
                 e0.record(self.x.stream)
             self.x.launch(l, self.k, pieces)
             if timed:  # end = this rank's part done on every internal stream (copy-engine variants too)
@@ -248,8 +249,11 @@ class ModuleBinding:
         """Gate every layer on the last finished iteration (end of a timed region);
         in graph mode this also joins the exchange streams back for capture."""
         if self.x.device_iteration:
+            cur = torch.cuda.current_stream(self.x.tr.device)
             for l in range(len(self.layers)):
-                self.x.join(l, torch.cuda.current_stream(self.x.tr.device))
+                self.x.join(l, cur)
+            if self._tstream is not None and torch.cuda.is_current_stream_capturing():
+                cur.wait_stream(self._tstream)  # the timing stream joined the capture too
         elif self.k > 0:
             for l in range(len(self.layers)):
                 self.x.gate(l, self.k - 1)

@@ -171,8 +171,8 @@ def _cifar10_quick():
 
         def forward(self, x):
             x = torch.relu(torch.max_pool2d(self.conv1(x), 3, 2, ceil_mode=True))
-            x = torch.avg_pool2d(torch.relu(self.conv2(x)), 3, 2, ceil_mode=True)
-            x = torch.avg_pool2d(torch.relu(self.conv3(x)), 3, 2, ceil_mode=True)
+            x = torch.nn.functional.avg_pool2d(torch.relu(self.conv2(x)), 3, 2, ceil_mode=True)
+            x = torch.nn.functional.avg_pool2d(torch.relu(self.conv3(x)), 3, 2, ceil_mode=True)
             return self.ip2(self.ip1(x.flatten(1)))
 
         def layers(self):
