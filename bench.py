@@ -49,7 +49,8 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    p.add_argument("--variant", default="twoshot", choices=["twoshot", "tree", "twoshot_ce", "auto"])
+    p.add_argument("--variant", default="twoshot", choices=["twoshot", "tree", "twoshot_ce", "auto", "nccl_bulk", "ddp"],
+                   help="nccl_bulk / ddp are comparison rows (NCCL on the path), not the product")
     p.add_argument("--chunk-elems", type=int, default=16384)
     p.add_argument("--max-ctas", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
@@ -415,7 +416,8 @@ def pgx_arm(args):
     if avg:
         ach = hbm / (avg / 1e3) / 1e9
         peak, peak_src = hbm_peak()
-        kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local", "tree": "k_tree_up"}.get(args.variant, "")
+        kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local + copy-engine transfers",
+                 "tree": "k_tree_up/k_tree_down"}[xchg.variants[L_DOM]]
         roof = {"bound": "hbm", "kernel": "%s (layer %d, %d params: fold + fused momentum update%s)" %
                 (kname, L_DOM, sizes[L_DOM], " + peer transfers" if world > 1 else ""), "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": None, "algorithmic_bytes_per_launch": hbm,
@@ -452,6 +454,98 @@ def pgx_arm(args):
         dist.destroy_process_group()
 
 
+def comparison_arm(args):
+    """Comparison rows only: the phase-separated bulk schedule (full backward,
+    one NCCL all-reduce of the flat gradient, then the libpgx fused update kernel), and
+    PyTorch DDP (bucketed NCCL all-reduce overlapped with backward) + fused torch SGD."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_00095_b200 import _lib
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("cpu:gloo,cuda:nccl", rank=rank, world_size=world, device_id=dev)
+    torch.backends.cudnn.benchmark = True
+    wl = wl_of(args)
+    model = wl["cls"]().to(dev)
+    h = wl["hyper"]
+    B = global_batch(wl, world) // world
+    gb = B * world
+    IMG = wl["image"]
+    g = torch.Generator().manual_seed(42 + rank)
+    dev_x = torch.randint(0, 256, (B, 3, IMG, IMG), dtype=torch.uint8, generator=g).to(dev)
+    dev_y = torch.randint(0, 1000, (B,), dtype=torch.int64, generator=g).to(dev)
+    params = [p for _, ps in model.layers() for p in ps]
+    n = sum(p.numel() for p in params)
+    if args.variant == "ddp":
+        net = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], gradient_as_bucket_view=True)
+        opt = torch.optim.SGD(params, lr=h["lr"], momentum=h["momentum"], weight_decay=h["weight_decay"],
+                              fused=True)
+    else:
+        net = model
+        flat_w = torch.empty(n, device=dev)
+        flat_g = torch.zeros(n, device=dev)
+        flat_v = torch.zeros(n, device=dev)
+        off = 0
+        with torch.no_grad():
+            for p in params:
+                flat_w[off:off + p.numel()].copy_(p.reshape(-1))
+                p.data = flat_w[off:off + p.numel()].view_as(p)
+                p.grad = flat_g[off:off + p.numel()].view_as(p)
+                off += p.numel()
+        dist.broadcast(flat_w, 0)
+
+    def step():
+        xin = dev_x.to(torch.bfloat16, memory_format=torch.channels_last).sub_(128.0).mul_(1.0 / 64.0)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            out = net(xin)
+        loss = model.loss(out, dev_y)
+        if args.variant == "ddp":
+            opt.zero_grad(set_to_none=False)
+            loss.backward()
+            opt.step()
+        else:
+            flat_g.zero_()
+            loss.backward()
+            dist.all_reduce(flat_g)  # bulk: one NCCL all-reduce after the whole backward
+            parts = (C.c_void_p * 1)(flat_g.data_ptr())
+            _lib.call("pgx_fold_update", _lib.MODE_FAST32, parts, 1, flat_w.data_ptr(), flat_v.data_ptr(), n,
+                      h["lr"], 1.0 / world, h["momentum"], h["weight_decay"],
+                      torch.cuda.current_stream().cuda_stream)
+        return loss
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=dist.new_group(backend="gloo"))
+    ms = float(t.item())
+    if rank == 0:
+        cfg = workload_config(world, args)
+        cfg["comparison"] = {"nccl_bulk": "phase-separated: backward, NCCL all-reduce of the flat gradient, "
+                                          "libpgx fused update (barrier.py schedule)",
+                             "ddp": "torch DDP bucketed NCCL all-reduce + fused torch SGD"}[args.variant]
+        print(json.dumps({"metric": wl["metric"], "value": gb * args.steps / (ms / 1e3), "unit": "images/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": wl["scaling"],
+                          "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+                          "impl": "comparison-" + args.variant}), flush=True)
+    dist.destroy_process_group()
+
+
 def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -464,6 +558,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         reference_arm(args)
+    elif args.variant in ("nccl_bulk", "ddp"):
+        comparison_arm(args)
     else:
         pgx_arm(args)
 

@@ -27,11 +27,16 @@ VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32}
 
 
-def choose_variant(elems: int, world: int, tree_below: int = 0) -> str:
-    """Layer-size policy: two-shot (reduce-scatter + all-gather) everywhere by default;
-    layers smaller than `tree_below` elements use the paper's tree."""
+def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20) -> str:
+    """Layer-size policy (measured, profiles/r1*_sweep*): small layers are latency-bound and
+    go through the SM two-shot kernel (fewest hops, ~26 us at 4 KB on 2 GPUs); layers of
+    `ce_from` elements or more move their shards with the copy engines, which do not take
+    SMs away from the backward kernels they overlap with.  `tree_below` optionally keeps
+    the paper's tree for the smallest layers."""
     if world > 1 and elems < tree_below:
         return "tree"
+    if world > 1 and elems >= ce_from:
+        return "twoshot_ce"
     return "twoshot"
 
 
