@@ -410,6 +410,9 @@ def pgx_arm(args):
             iso.append(e0.elapsed_time(e1))
         bind.k += 10
 
+    # ---- timeline: a few traced eager steps, reference CSV schema + overlap ----
+    timeline = trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world)
+
     nvl, hbm = xchg.layer_bytes(L_DOM)
     avg = statistics.mean(durs) if durs else None
     roof = None
@@ -433,7 +436,7 @@ def pgx_arm(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
-            "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None}
+            "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None, "timeline": timeline}
     if args.per_gpu_batch:
         line["config"]["per_gpu_batch"] = B
         line["config"]["global_batch"] = gb
@@ -452,6 +455,51 @@ def pgx_arm(args):
     tr.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world, steps=3):
+    """Per-layer exchange spans vs forward/backward on the device clock (CUDA events), in
+    the reference's timeline schema (timeline.py:34) and its overlap ratio (timeline.py:137)."""
+    import torch
+
+    from paper_1706_00095_b200.timeline import Recorder, compute_overlap, write_timeline_csv
+
+    rec = Recorder(rank)
+    bind.trace = []
+    marks = []
+    for _ in range(steps):
+        k = bind.k
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        xin = dev_x.to(torch.bfloat16, memory_format=torch.channels_last).sub_(128.0).mul_(1.0 / 64.0)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            out = model(xin)
+        loss = model.loss(out, dev_y)
+        ev[1].record()
+        loss.backward()
+        ev[2].record()
+        bind.step_done()
+        marks.append((k, ev))
+    bind.drain()
+    torch.cuda.synchronize()
+    t0 = marks[0][1][0]
+    ns = lambda e: int(t0.elapsed_time(e) * 1e6)  # noqa: E731
+    for k, ev in marks:
+        rec.record("forward", k, -1, ns(ev[0]), ns(ev[1]))
+        rec.record("backward_layer", k, -1, ns(ev[1]), ns(ev[2]))
+    tails = []
+    for k, l, r0, e1 in bind.trace:
+        rec.record("send_trigger", k, l, ns(r0), ns(e1))
+    for k, ev in marks:
+        ends = [ns(e1) for kk, l, r0, e1 in bind.trace if kk == k]
+        tails.append(max(0, max(ends) - ns(ev[2])) / 1e6 if ends else 0.0)
+    bind.trace = None
+    path = args.timeline or ""
+    if path:
+        write_timeline_csv(rec.events, path.replace("{rank}", str(rank)))
+    return {"overlap_ratio": compute_overlap(rec.events), "steps_traced": steps,
+            "exchange_tail_after_backward_ms": statistics.mean(tails), "schema": "timeline.py:34 CSV",
+            "csv": path or None}
 
 
 def comparison_arm(args):

@@ -120,8 +120,15 @@ class DeviceExchange:
                 raise ShapeError("gradient pieces must be contiguous")
         ptrs = (C.c_void_p * n)(*[p.data_ptr() for p in pieces])
         cnts = (C.c_uint64 * n)(*[p.numel() for p in pieces])
-        s = (stream or self.stream).cuda_stream
-        _lib.call("pgx_xchg_layer", self.handle, layer, iteration & 0xFFFFFFFF, ptrs, cnts, n, phases, s)
+        st = stream or self.stream
+        _lib.call("pgx_xchg_layer", self.handle, layer, iteration & 0xFFFFFFFF, ptrs, cnts, n, phases, st.cuda_stream)
+        if not torch.cuda.is_current_stream_capturing():
+            # the pieces are read asynchronously on the launch stream and, for the copy-engine
+            # variant, on internal streams: keep the caching allocator from recycling them early
+            for p in pieces:
+                p.record_stream(st)
+                for s in self.internal_streams:
+                    p.record_stream(s)
         self.launches += 1
 
     def set_device_iteration(self, enable: bool, current: int) -> None:
@@ -191,6 +198,7 @@ class ModuleBinding:
         self.gpu_launches = 0
         self.timed_layers: set = set()   # layers whose launches are bracketed by CUDA events
         self._tstream = None
+        self.trace = None                # list -> record (iteration, layer, ready_event, done_event)
         self.events: dict = {}
 
     def _make_hook(self, l):
@@ -207,12 +215,11 @@ class ModuleBinding:
                 g = p.grad
                 if not g.is_contiguous():
                     g = g.contiguous()
-                if not self.x.device_iteration:  # graph replays keep their pool alive
-                    g.record_stream(self.x.stream)
-                    for st in self.x.internal_streams:  # copy-engine variants read it there
-                        g.record_stream(st)
-                pieces.append(g)
-            timed = l in self.timed_layers
+                pieces.append(g)  # DeviceExchange.launch ties their lifetime to its streams
+            if self.trace is not None:  # timeline: gradient ready (compute stream) .. layer exchanged
+                r0 = torch.cuda.Event(enable_timing=True)
+                r0.record(compute)
+            timed = l in self.timed_layers or self.trace is not None
             if timed:  # external events become event-record nodes when captured in a graph
                 ext = torch.cuda.is_current_stream_capturing()
                 e0 = torch.cuda.Event(enable_timing=True, external=ext)
@@ -224,7 +231,10 @@ class ModuleBinding:
                     self._tstream = torch.cuda.Stream(device=self.x.tr.device)
                 self.x.join(l, self._tstream)
                 e1.record(self._tstream)
-                self.events.setdefault(l, []).append((e0, e1))
+                if l in self.timed_layers:
+                    self.events.setdefault(l, []).append((e0, e1))
+                if self.trace is not None:
+                    self.trace.append((self.k, l, r0, e1))
             for p in params:
                 p.grad = None  # next backward allocates fresh gradients; the allocator
                 # keeps these alive until the exchange stream is past them

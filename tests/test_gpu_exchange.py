@@ -216,3 +216,29 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant):
     bind.remove()
     x.close()
     world.close()
+
+
+@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce"])
+def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
+    """Layers smaller than one vector per rank (empty owner shards), ragged tails and a
+    piece boundary inside a vector, 8 ranks stepped on one GPU, ref32 bit-exact."""
+    elems = [1, 3, 5, 17, 33, 4097]
+    N = 8
+    world, trs, xs = build(N, elems, "ref32", variant, chunk_elems=8, lr=0.125)
+    w = [O.seeded_fill(9 ^ l, n, 1.0).astype(np.float32) for l, n in enumerate(elems)]
+    for x in xs:
+        for l in range(len(elems)):
+            x.layer_views[l].copy_(torch.from_numpy(w[l]))
+    torch.cuda.synchronize()
+    for k in range(2):
+        for l in reversed(range(len(elems))):
+            n = elems[l]
+            grads = [O.seeded_fill(O.derived_seed(3, r, l, k), n, 1.0).astype(np.float32) for r in range(N)]
+            pieces = [split_pieces(torch.from_numpy(g).cuda(), n // 2) for g in grads]
+            stepped_layer(xs, trs, l, k, pieces)
+            w[l] = O.exchange_iteration(grads, w[l], 0.125, "ref32")
+            for r in range(N):
+                assert xs[r].layer_views[l].cpu().numpy().tobytes() == w[l].tobytes(), (variant, k, l, r)
+    for x in xs:
+        x.close()
+    world.close()
