@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    p.add_argument("--variant", default="twoshot", choices=["twoshot", "tree", "twoshot_ce", "auto", "nccl_bulk", "ddp"],
+    p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "auto", "nccl_bulk", "ddp"],
                    help="nccl_bulk / ddp are comparison rows (NCCL on the path), not the product")
     p.add_argument("--chunk-elems", type=int, default=16384)
     p.add_argument("--max-ctas", type=int, default=0)
