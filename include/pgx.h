@@ -211,6 +211,9 @@ int pgx_xchg_tick(pgx_xchg* x, void* stream);
 /* Internal streams (0 = tree down pass, 1 = CE reduce-scatter, 2 = CE owner side),
  * so callers can tie gradient lifetimes to them. */
 int pgx_xchg_stream(pgx_xchg* x, int which, void** stream_out);
+/* Replace the internal streams by caller-owned ones (e.g. framework streams whose
+ * lifetime the framework's allocator tracks); the library will not destroy them. */
+int pgx_xchg_set_streams(pgx_xchg* x, void* down, void* ce_rs, void* ce_own);
 /* Make `stream` wait until layer l's local exchange work (own shard, side
  * streams) finished — joins every internal stream back (graph capture). */
 int pgx_xchg_join(pgx_xchg* x, int layer, void* stream);

@@ -88,6 +88,7 @@ SIGNATURES = {
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],
+    "pgx_xchg_set_streams": [vp, vp, vp, vp],
     "pgx_xchg_join": [vp, i32, vp],
     "pgx_xchg_device_iteration": [vp, i32, u32],
     "pgx_xchg_tick": [vp, vp],

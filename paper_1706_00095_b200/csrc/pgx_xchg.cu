@@ -547,6 +547,7 @@ struct pgx_xchg {
   uint64_t launches = 0;
   cudaStream_t down = nullptr;
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
+  bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
   std::vector<XEvent> rs_done, down_done;          // side-stream completion (joins for graph capture)
@@ -859,9 +860,11 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   for (auto& e : x->rs_done) cudaEventDestroy(e.e);
   for (auto& e : x->down_done) cudaEventDestroy(e.e);
   if (x->iter_dev) cudaFree(x->iter_dev);
-  if (x->down) cudaStreamDestroy(x->down);
-  if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
-  if (x->ce_own) cudaStreamDestroy(x->ce_own);
+  if (x->own_streams) {
+    if (x->down) cudaStreamDestroy(x->down);
+    if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
+    if (x->ce_own) cudaStreamDestroy(x->ce_own);
+  }
   cudaSetDevice(prev);
   delete x;  // segments belong to the world
   return PGX_OK;
@@ -1015,6 +1018,25 @@ int pgx_xchg_tick(pgx_xchg* x, void* stream) {
   cudaError_t e = cudaGetLastError();
   if (prev != x->dev) cudaSetDevice(prev);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "tick: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
+int pgx_xchg_set_streams(pgx_xchg* x, void* down, void* ce_rs, void* ce_own) {
+  if (!down || !ce_rs || !ce_own) return fail(PGX_E_CONFIG, "three streams required");
+  int prev;
+  cudaGetDevice(&prev);
+  cudaSetDevice(x->dev);
+  cudaDeviceSynchronize();
+  if (x->own_streams) {
+    cudaStreamDestroy(x->down);
+    cudaStreamDestroy(x->ce_rs);
+    cudaStreamDestroy(x->ce_own);
+  }
+  cudaSetDevice(prev);
+  x->down = (cudaStream_t)down;
+  x->ce_rs = (cudaStream_t)ce_rs;
+  x->ce_own = (cudaStream_t)ce_own;
+  x->own_streams = false;
   return PGX_OK;
 }
 

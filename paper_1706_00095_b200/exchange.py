@@ -89,11 +89,11 @@ class DeviceExchange:
         self.connected = False
         self.device_iteration = False
         self.launches = 0
-        self.internal_streams = []
-        for which in range(3):
-            sp = C.c_void_p()
-            _lib.call("pgx_xchg_stream", h, which, C.byref(sp))
-            self.internal_streams.append(torch.cuda.ExternalStream(sp.value, device=transport.device))
+        # The library's side streams (tree down pass, copy-engine push, owner side) are torch
+        # streams, so the caching allocator can track gradient pieces used on them.
+        with torch.cuda.device(transport.device):
+            self.internal_streams = [torch.cuda.Stream(device=transport.device, priority=-1) for _ in range(3)]
+        _lib.call("pgx_xchg_set_streams", h, *[s.cuda_stream for s in self.internal_streams])
 
     # -- wiring ----------------------------------------------------------------
     def connect(self) -> None:
