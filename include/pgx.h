@@ -74,6 +74,9 @@ int pgx_segment_attach_ipc(pgx_world* w, int peer, uint32_t seg_id, const void* 
                            uint64_t size, uint32_t notif_count);
 int pgx_segment_attach_local(pgx_world* w, int peer, uint32_t seg_id, void* data,
                              uint32_t* flags, uint64_t size, uint32_t notif_count);
+/* Several ranks on distinct GPUs inside ONE process (host-stepped multi-GPU tests and
+ * per-phase microbenchmarks): let `device` address `peer`'s memory directly. */
+int pgx_enable_peer_access(int device, int peer);
 
 /* ------------------------------------------------------------ data plane
  * write_notify (inproc.py:134-142, base.py:217-225 validation): copy `size`

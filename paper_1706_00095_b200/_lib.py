@@ -61,6 +61,7 @@ SIGNATURES = {
     "pgx_segment_export": [vp, u32, vp],
     "pgx_segment_attach_ipc": [vp, i32, u32, vp, u64, u32],
     "pgx_segment_attach_local": [vp, i32, u32, vp, vp, u64, u32],
+    "pgx_enable_peer_access": [i32, i32],
     "pgx_write_notify": [vp, u32, u64, i32, u32, u64, u64, u32, u32, vp],
     "pgx_write_notify_chunked": [vp, u32, u64, i32, u32, u64, u64, u64, u32, u32, vp],
     "pgx_notify_poll": [vp, u32, u32, u32, P(u32), P(u32), u32, P(u32)],

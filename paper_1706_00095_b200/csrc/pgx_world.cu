@@ -207,6 +207,20 @@ int pgx_world_destroy(pgx_world* w) {
   return PGX_OK;
 }
 
+int pgx_enable_peer_access(int device, int peer) {
+  DeviceGuard g(device);
+  int can = 0;
+  PGX_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return fail(PGX_E_ROUTING, "device %d cannot access device %d", device, peer);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return PGX_OK;
+  }
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
 int pgx_world_status(pgx_world* w, uint32_t* s) {
   *s = *(volatile uint32_t*)w->status_host;
   return PGX_OK;

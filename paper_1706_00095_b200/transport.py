@@ -312,7 +312,7 @@ class LocalTransport(CudaTransport):
     def __init__(self, world: "LocalWorld", rank: int):
         self._world = world
         self.inline = world.inline
-        super().__init__(rank, world.world_size, world.device_index)
+        super().__init__(rank, world.world_size, world.device_of(rank))
 
     def _on_segment_created(self, seg: Segment) -> None:
         self._world._publish(self.rank, seg)
@@ -333,7 +333,8 @@ class LocalWorld:
     so writes are device stores into the peer rank's memory on the same GPU.
     """
 
-    def __init__(self, world_size: int, latency: LatencyModel | None = None, device: int = 0, inline: bool = True):
+    def __init__(self, world_size: int, latency: LatencyModel | None = None, device: int = 0, inline: bool = True,
+                 devices=None):
         if world_size < 1:
             raise ConfigError(f"world size must be >= 1, got {world_size}")
         if latency is not None and not latency.is_zero:
@@ -341,10 +342,22 @@ class LocalWorld:
         self.world_size = world_size
         self.device_index = device
         self.inline = inline
+        # optional rank -> GPU map: several GPUs driven from one process (peer access enabled)
+        self.devices = list(devices) if devices is not None else None
+        if self.devices is not None:
+            if len(self.devices) != world_size:
+                raise ConfigError("one device per rank")
+            for a in set(self.devices):
+                for b in set(self.devices):
+                    if a != b:
+                        _lib.call("pgx_enable_peer_access", a, b)
         self._transports: dict[int, LocalTransport] = {}
         self._segs: list[tuple[int, Segment]] = []
         self._barrier = threading.Barrier(world_size)
         self._lock = threading.Lock()
+
+    def device_of(self, rank: int) -> int:
+        return self.devices[rank] if self.devices is not None else self.device_index
 
     def transport(self, rank: int) -> LocalTransport:
         if not (0 <= rank < self.world_size):
