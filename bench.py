@@ -396,22 +396,28 @@ def pgx_arm(args):
         durs = [a.elapsed_time(b_) for a, b_ in bind.events.get(L_DOM, [])]
     bind.timed_layers = set()
 
-    # ---- dominant kernel in isolation (same launch, no concurrent backward) ----
-    gfc6 = [torch.randn_like(p) * 1e-3 for p in model.layers()[L_DOM][1]]
-    iso = []
-    if world == 1:
-        for i in range(10):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(xchg.stream)
-            xchg.launch(L_DOM, bind.k + i, gfc6)
-            xchg.join(L_DOM, xchg.stream)
-            e1.record(xchg.stream)
-            torch.cuda.synchronize()
-            iso.append(e0.elapsed_time(e1))
-        bind.k += 10
-
     # ---- timeline: a few traced eager steps, reference CSV schema + overlap ----
     timeline = trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world)
+
+    # ---- dominant layer's exchange in isolation (same launch, no concurrent backward): every
+    # rank, device flag barrier before each, launch -> own part done -> gate on all arrivals.
+    # Runs last: it advances only this layer's epochs. ----
+    gfc6 = [torch.randn_like(p) * 1e-3 for p in model.layers()[L_DOM][1]]
+    iso = []
+    for i in range(10):
+        tr.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(xchg.stream)
+        xchg.launch(L_DOM, bind.k + i, gfc6)
+        xchg.join(L_DOM, xchg.stream)
+        xchg.gate(L_DOM, bind.k + i, stream=xchg.stream)
+        e1.record(xchg.stream)
+        torch.cuda.synchronize()
+        iso.append(e0.elapsed_time(e1))
+    if world > 1:
+        t = torch.tensor([statistics.median(iso)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        iso = [float(t.item())]
 
     nvl, hbm = xchg.layer_bytes(L_DOM)
     avg = statistics.mean(durs) if durs else None
@@ -428,7 +434,7 @@ def pgx_arm(args):
                 "launch_share_of_step": avg / (ms / args.steps),
                 "measured_in": ("CUDA events captured in the step graph, %d replays after the timed region"
                                 % len(durs)) if graph is not None else "CUDA events in every timed eager step"}
-        if iso:
+        if iso and world == 1:
             roof["isolated_launch_ms"] = statistics.median(iso)
             roof["isolated_achieved"] = hbm / (statistics.median(iso) / 1e3) / 1e9
             roof["isolated_frac"] = roof["isolated_achieved"] / peak
@@ -442,9 +448,14 @@ def pgx_arm(args):
         line["config"]["global_batch"] = gb
         line["config"]["diagnostic"] = "per-GPU batch overridden; not the headline configuration"
     if world > 1 and avg:
+        iso_ms = statistics.median(iso)
         line["roofline_nvlink"] = {"bound": "nvlink", "achieved": nvl / (avg / 1e3) / 1e9, "peak": NVLINK_PEAK_GBS,
                                    "unit": "GB/s", "frac": nvl / (avg / 1e3) / 1e9 / NVLINK_PEAK_GBS,
-                                   "bytes_per_launch": nvl, "peak_source": "B200_PROFILING.md measured peer copy"}
+                                   "bytes_per_launch": nvl, "peak_source": "B200_PROFILING.md measured peer copy",
+                                   "what": "dominant layer's whole exchange (RS + fold/update + AG + arrival), "
+                                           "this rank's out-bytes over its in-step duration",
+                                   "isolated_ms": iso_ms, "isolated_achieved": nvl / (iso_ms / 1e3) / 1e9,
+                                   "isolated_frac": nvl / (iso_ms / 1e3) / 1e9 / NVLINK_PEAK_GBS}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_step_timing(world, seconds=args.cpu_seconds, workload=args.workload)
     if rank == 0:

@@ -211,12 +211,14 @@ int pgx_xchg_gate(pgx_xchg* x, int layer, uint32_t iteration, void* stream);
  * iteration (forward-pre-hook gate), 0 = the current one (end-of-step drain). */
 int pgx_xchg_device_iteration(pgx_xchg* x, int enable, uint32_t current);
 int pgx_xchg_tick(pgx_xchg* x, void* stream);
-/* Internal streams (0 = tree down pass, 1 = CE reduce-scatter, 2 = CE owner side),
- * so callers can tie gradient lifetimes to them. */
+/* Internal streams (0 = tree down pass, 1 = CE reduce-scatter, 2 = CE owner side,
+ * 3 = CE all-gather, 4 = CE second push stream). */
 int pgx_xchg_stream(pgx_xchg* x, int which, void** stream_out);
 /* Replace the internal streams by caller-owned ones (e.g. framework streams whose
- * lifetime the framework's allocator tracks); the library will not destroy them. */
-int pgx_xchg_set_streams(pgx_xchg* x, void* down, void* ce_rs, void* ce_own);
+ * lifetime the framework's allocator tracks); the library will not destroy them.
+ * Order: tree down pass, CE push, CE owner, CE all-gather, CE second push. */
+#define PGX_XCHG_STREAMS 5
+int pgx_xchg_set_streams(pgx_xchg* x, void* const* streams, int n);
 /* Make `stream` wait until layer l's local exchange work (own shard, side
  * streams) finished — joins every internal stream back (graph capture). */
 int pgx_xchg_join(pgx_xchg* x, int layer, void* stream);

@@ -21,6 +21,7 @@ IPC_HANDLE_BYTES = 64
 CONTROL_SEGMENT = 15
 MAX_RANKS = 8
 MAX_PIECES = 4
+XCHG_STREAMS = 5
 
 MODE_REF64, MODE_REF32, MODE_FAST32 = 0, 1, 2
 VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE = 0, 1, 2
@@ -89,7 +90,7 @@ SIGNATURES = {
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],
-    "pgx_xchg_set_streams": [vp, vp, vp, vp],
+    "pgx_xchg_set_streams": [vp, P(vp), i32],
     "pgx_xchg_join": [vp, i32, vp],
     "pgx_xchg_device_iteration": [vp, i32, u32],
     "pgx_xchg_tick": [vp, vp],

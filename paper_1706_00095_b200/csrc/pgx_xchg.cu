@@ -77,6 +77,7 @@ struct XArgs {
   int rank, world, parity, K;          // K: rx slots per parity
   uint32_t push_items, items;
   uint32_t item_begin, item_end;       // claimed range (phase selection)
+  uint64_t olo, ohi;                   // TWOSHOT_CE owner sub-range (ohi == 0: the whole shard)
   const uint32_t* iter;                // device iteration counter (graph mode) or null
   double lr;
   float scale, mu, wd;
@@ -471,9 +472,15 @@ __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
   constexpr int W = VecT<T>::W;
   constexpr int U = N <= 4 ? 2 : 1;
   const int me = a.rank;
-  uint64_t lo = min((uint64_t)me * a.sl, a.S), hi = min((uint64_t)(me + 1) * a.sl, a.S);
+  const uint64_t base = min((uint64_t)me * a.sl, a.S);
+  uint64_t lo = base, hi = min((uint64_t)(me + 1) * a.sl, a.S);
+  if (a.ohi) {
+    lo = a.olo;
+    hi = a.ohi;
+  }
   if (lo >= hi) return;
-  const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl;
+  // receive slots are indexed from the shard start; owner_vectors indexes them by q
+  const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl + (lo - base);
   const uint64_t nvec = (hi - lo + W - 1) / W, span = (uint64_t)U * blockDim.x;
   for (uint64_t blk = blockIdx.x; blk * span < nvec; blk += gridDim.x)
     owner_vectors<N, T, U, false>(a, rxb, lo, hi, blk * span + threadIdx.x, nvec);
@@ -547,10 +554,14 @@ struct pgx_xchg {
   uint64_t launches = 0;
   cudaStream_t down = nullptr;
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
+  cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
+  int ce_parts = 1, ce_rs_streams = 1;             // owner pipelining depth, push streams
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
   std::vector<XEvent> rs_done, down_done;          // side-stream completion (joins for graph capture)
+  std::vector<XEvent> rs2_done;
+  std::vector<std::vector<XEvent>> part_ev;        // TWOSHOT_CE owner parts ready for their all-gather
   uint32_t* iter_dev = nullptr;                    // device iteration counter (graph mode)
   bool device_iter = false;
   uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
@@ -650,9 +661,14 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
   cudaError_t e = xrecord(x->ready[l], s);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
   if (phases & PGX_PHASE_PUSH) {
-    xwait(x->ce_rs, x->ready[l]);
+    // peers alternate between one or two copy streams; each stream signals its own peers
+    const int ns = (x->ce_rs_streams > 1 && N > 2) ? 2 : 1;
+    cudaStream_t rs[2] = {x->ce_rs, x->ce_rs2};
+    FlagOut fo[2] = {};
+    for (int q = 0; q < ns; ++q) xwait(rs[q], x->ready[l]);
     for (int d = 1; d < N; ++d) {
       int j = (me + d) % N;
+      cudaStream_t cs = rs[(d - 1) % ns];
       uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
       uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * P.sl) * esz;
       uint64_t pb = 0;
@@ -661,19 +677,21 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
         uint64_t ol = std::max(lo, pb), oh = std::min(hi, pe);
         if (ol < oh) {
           e = cudaMemcpyAsync(dst + (ol - lo) * esz, static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz,
-                              (oh - ol) * esz, cudaMemcpyDeviceToDevice, x->ce_rs);
+                              (oh - ol) * esz, cudaMemcpyDeviceToDevice, cs);
           if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
         }
         pb = pe;
       }
+      FlagOut& f = fo[(d - 1) % ns];
+      f.f[f.n++] = a.rxflags[j] + (uint64_t)me * P.C;
     }
-    FlagOut fo{};
-    for (int d = 1; d < N; ++d) fo.f[fo.n++] = a.rxflags[(me + d) % N] + (uint64_t)me * P.C;
-    if (fo.n) {
-      k_signal<<<1, 32, 0, x->ce_rs>>>(fo, a.epoch, a.iter);
-      ++x->launches;
+    for (int q = 0; q < ns; ++q) {
+      if (fo[q].n) {
+        k_signal<<<1, 32, 0, rs[q]>>>(fo[q], a.epoch, a.iter);
+        ++x->launches;
+      }
+      xrecord(q == 0 ? x->rs_done[l] : x->rs2_done[l], rs[q]);
     }
-    xrecord(x->rs_done[l], x->ce_rs);
   }
   if (phases & PGX_PHASE_OWNER) {
     xwait(x->ce_own, x->ready[l]);
@@ -685,29 +703,43 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
       k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
       ++x->launches;
     }
-    int grid = std::max(1, std::min(P.grid, (int)((P.sl / VecT<float>::W + kThreads - 1) / kThreads)));
-    if (esz == 8)
-      launch_owner_local<double>(N, grid, x->ce_own, a);
-    else
-      launch_owner_local<float>(N, grid, x->ce_own, a);
-    ++x->launches;
-    uint64_t lo = std::min(P.S, (uint64_t)me * P.sl), hi = std::min(P.S, (uint64_t)(me + 1) * P.sl);
-    for (int d = 1; d < N; ++d) {
-      int t = (me + d) % N;
-      if (lo < hi) {
-        e = cudaMemcpyAsync(static_cast<uint8_t*>(a.model[t]) + lo * esz, static_cast<uint8_t*>(a.model[me]) + lo * esz,
-                            (hi - lo) * esz, cudaMemcpyDeviceToDevice, x->ce_own);
+    const uint64_t lo = std::min(P.S, (uint64_t)me * P.sl), hi = std::min(P.S, (uint64_t)(me + 1) * P.sl);
+    // owner fold/update in parts; each part's all-gather copies start as soon as it is done
+    int parts = N > 1 ? x->ce_parts : 1;
+    const uint64_t min_part = 1u << 18;  // elements: do not split small shards
+    while (parts > 1 && (hi - lo) / parts < min_part) --parts;
+    for (int p = 0; p < parts; ++p) {
+      uint64_t plo = lo + ((hi - lo) * p / parts) / 4 * 4, phi = p + 1 == parts ? hi : lo + ((hi - lo) * (p + 1) / parts) / 4 * 4;
+      a.olo = plo;
+      a.ohi = phi;
+      int grid = std::max(1, std::min(P.grid, (int)(((phi - plo) / VecT<float>::W + kThreads - 1) / kThreads)));
+      if (phi > plo) {
+        if (esz == 8)
+          launch_owner_local<double>(N, grid, x->ce_own, a);
+        else
+          launch_owner_local<float>(N, grid, x->ce_own, a);
+        ++x->launches;
+      }
+      if (N == 1) continue;
+      xrecord(x->part_ev[l][p], x->ce_own);
+      xwait(x->ce_ag, x->part_ev[l][p]);
+      for (int d = 1; d < N && phi > plo; ++d) {
+        int t = (me + d) % N;
+        e = cudaMemcpyAsync(static_cast<uint8_t*>(a.model[t]) + plo * esz, static_cast<uint8_t*>(a.model[me]) + plo * esz,
+                            (phi - plo) * esz, cudaMemcpyDeviceToDevice, x->ce_ag);
         if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
       }
     }
+    cudaStream_t tail = N > 1 ? x->ce_ag : x->ce_own;
+    if (N == 1 || lo >= hi) xwait(x->ce_ag, x->ready[l]);  // keep ce_ag joined even with nothing to copy
     FlagOut fo{};
     for (int d = 1; d < N; ++d)
       fo.f[fo.n++] = a.mflags[(me + d) % N] + x->ownerflag_base + (uint64_t)l * N + me;
     if (fo.n) {
-      k_signal<<<1, 32, 0, x->ce_own>>>(fo, a.epoch, a.iter);
+      k_signal<<<1, 32, 0, tail>>>(fo, a.epoch, a.iter);
       ++x->launches;
     }
-    e = xrecord(x->done[l], x->ce_own);
+    e = xrecord(x->done[l], tail);
     if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
   }
   return PGX_OK;
@@ -824,15 +856,24 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->down, cudaStreamNonBlocking, hi_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs, cudaStreamNonBlocking, hi_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_own, cudaStreamNonBlocking, hi_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_ag, cudaStreamNonBlocking, hi_prio);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs2, cudaStreamNonBlocking, hi_prio);
+    if (const char* v = getenv("PGX_CE_PARTS")) x->ce_parts = std::max(1, std::min(8, atoi(v)));
+    if (const char* v = getenv("PGX_CE_RS_STREAMS")) x->ce_rs_streams = std::max(1, std::min(2, atoi(v)));
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
     x->rs_done.resize(cfg->num_layers);
+    x->rs2_done.resize(cfg->num_layers);
     x->down_done.resize(cfg->num_layers);
+    x->part_ev.resize(cfg->num_layers, std::vector<XEvent>(8));
     for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l) {
       e = cudaEventCreateWithFlags(&x->done[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ready[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs_done[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->down_done[l].e, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs2_done[l].e, cudaEventDisableTiming);
+      for (int p = 0; p < 8 && e == cudaSuccess; ++p)
+        e = cudaEventCreateWithFlags(&x->part_ev[l][p].e, cudaEventDisableTiming);
     }
     if (e == cudaSuccess) e = cudaMalloc(&x->iter_dev, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(x->iter_dev, 0xFF, sizeof(uint32_t));
@@ -859,11 +900,16 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   for (auto& e : x->ready) cudaEventDestroy(e.e);
   for (auto& e : x->rs_done) cudaEventDestroy(e.e);
   for (auto& e : x->down_done) cudaEventDestroy(e.e);
+  for (auto& e : x->rs2_done) cudaEventDestroy(e.e);
+  for (auto& v : x->part_ev)
+    for (auto& e : v) cudaEventDestroy(e.e);
   if (x->iter_dev) cudaFree(x->iter_dev);
   if (x->own_streams) {
     if (x->down) cudaStreamDestroy(x->down);
     if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
     if (x->ce_own) cudaStreamDestroy(x->ce_own);
+    if (x->ce_ag) cudaStreamDestroy(x->ce_ag);
+    if (x->ce_rs2) cudaStreamDestroy(x->ce_rs2);
   }
   cudaSetDevice(prev);
   delete x;  // segments belong to the world
@@ -974,6 +1020,7 @@ int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
   if (prev != x->dev) cudaSetDevice(x->dev);
   cudaError_t e = xwait(s, x->done[l]);
   if (e == cudaSuccess) e = xwait(s, x->rs_done[l]);
+  if (e == cudaSuccess) e = xwait(s, x->rs2_done[l]);
   if (e == cudaSuccess) e = xwait(s, x->down_done[l]);
   const uint32_t* it = x->device_iter ? x->iter_dev : nullptr;
   if (e == cudaSuccess && P.variant == PGX_VARIANT_TWOSHOT_CE) {
@@ -1021,8 +1068,10 @@ int pgx_xchg_tick(pgx_xchg* x, void* stream) {
   return PGX_OK;
 }
 
-int pgx_xchg_set_streams(pgx_xchg* x, void* down, void* ce_rs, void* ce_own) {
-  if (!down || !ce_rs || !ce_own) return fail(PGX_E_CONFIG, "three streams required");
+int pgx_xchg_set_streams(pgx_xchg* x, void* const* streams, int n) {
+  if (n != PGX_XCHG_STREAMS) return fail(PGX_E_CONFIG, "%d streams required, got %d", PGX_XCHG_STREAMS, n);
+  for (int i = 0; i < n; ++i)
+    if (!streams[i]) return fail(PGX_E_CONFIG, "stream %d is null", i);
   int prev;
   cudaGetDevice(&prev);
   cudaSetDevice(x->dev);
@@ -1031,18 +1080,23 @@ int pgx_xchg_set_streams(pgx_xchg* x, void* down, void* ce_rs, void* ce_own) {
     cudaStreamDestroy(x->down);
     cudaStreamDestroy(x->ce_rs);
     cudaStreamDestroy(x->ce_own);
+    cudaStreamDestroy(x->ce_ag);
+    cudaStreamDestroy(x->ce_rs2);
   }
   cudaSetDevice(prev);
-  x->down = (cudaStream_t)down;
-  x->ce_rs = (cudaStream_t)ce_rs;
-  x->ce_own = (cudaStream_t)ce_own;
+  x->down = (cudaStream_t)streams[0];
+  x->ce_rs = (cudaStream_t)streams[1];
+  x->ce_own = (cudaStream_t)streams[2];
+  x->ce_ag = (cudaStream_t)streams[3];
+  x->ce_rs2 = (cudaStream_t)streams[4];
   x->own_streams = false;
   return PGX_OK;
 }
 
 int pgx_xchg_stream(pgx_xchg* x, int which, void** out) {
-  cudaStream_t st[3] = {x->down, x->ce_rs, x->ce_own};
-  if (which < 0 || which > 2) return fail(PGX_E_RANGE, "stream index %d outside 0..2", which);
+  cudaStream_t st[PGX_XCHG_STREAMS] = {x->down, x->ce_rs, x->ce_own, x->ce_ag, x->ce_rs2};
+  if (which < 0 || which >= PGX_XCHG_STREAMS)
+    return fail(PGX_E_RANGE, "stream index %d outside 0..%d", which, PGX_XCHG_STREAMS - 1);
   *out = st[which];
   return PGX_OK;
 }
@@ -1051,6 +1105,7 @@ int pgx_xchg_join(pgx_xchg* x, int l, void* stream) {
   if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
   PGX_CUDA(xwait((cudaStream_t)stream, x->done[l]));
   PGX_CUDA(xwait((cudaStream_t)stream, x->rs_done[l]));
+  PGX_CUDA(xwait((cudaStream_t)stream, x->rs2_done[l]));
   PGX_CUDA(xwait((cudaStream_t)stream, x->down_done[l]));
   return PGX_OK;
 }

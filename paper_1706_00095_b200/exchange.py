@@ -92,8 +92,10 @@ class DeviceExchange:
         # The library's side streams (tree down pass, copy-engine push, owner side) are torch
         # streams, so the caching allocator can track gradient pieces used on them.
         with torch.cuda.device(transport.device):
-            self.internal_streams = [torch.cuda.Stream(device=transport.device, priority=-1) for _ in range(3)]
-        _lib.call("pgx_xchg_set_streams", h, *[s.cuda_stream for s in self.internal_streams])
+            self.internal_streams = [torch.cuda.Stream(device=transport.device, priority=-1)
+                                     for _ in range(_lib.XCHG_STREAMS)]
+        arr = (C.c_void_p * _lib.XCHG_STREAMS)(*[s.cuda_stream for s in self.internal_streams])
+        _lib.call("pgx_xchg_set_streams", h, arr, _lib.XCHG_STREAMS)
 
     # -- wiring ----------------------------------------------------------------
     def connect(self) -> None:
