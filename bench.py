@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "auto", "nccl_bulk", "ddp"],
                    help="nccl_bulk / ddp are comparison rows (NCCL on the path), not the product")
     p.add_argument("--chunk-elems", type=int, default=16384)
+    p.add_argument("--gate", default="auto", choices=["auto", "layer", "model"],
+                   help="per-layer forward gates, or one whole-model gate per step (auto: model if > 16 layers)")
     p.add_argument("--max-ctas", type=int, default=0)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager steps instead of a captured CUDA graph")
@@ -156,7 +158,7 @@ def workload_config(world, args):
             "parallelism": f"dp{world}", "exchange": args.variant, "update": f"fast32 momentum SGD lr {h['lr']} mu {h['momentum']} "
             f"wd {h['weight_decay']} scale 1/N", "fwd_bwd": "PyTorch cuDNN bf16 autocast, fp32 master weights/grads",
             "l2": "working set > L2 (244 MB fp32 weights + 244 MB grads + activations per step)",
-            "chunk_elems": args.chunk_elems, "step": "CUDA graph replay" if not args.no_graph else "eager"}
+            "chunk_elems": args.chunk_elems, "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager"}
 
 
 # ------------------------------------------------------------------ model
@@ -243,7 +245,8 @@ def pgx_arm(args):
     tr = DistTransport(rank, world, local, timeout_s=60.0)
     xchg = DeviceExchange(tr, sizes, mode="fast32", variant=args.variant, chunk_elems=args.chunk_elems,
                           scale=1.0 / world, max_ctas=args.max_ctas, **wl["hyper"])
-    bind = ModuleBinding(xchg, model.layers())
+    gate = args.gate if args.gate != "auto" else ("model" if len(sizes) > 16 else "layer")
+    bind = ModuleBinding(xchg, model.layers(), gate=gate)
     if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)
         flat = xchg.model.cpu()
         dist.broadcast(flat, 0)

@@ -224,6 +224,9 @@ int pgx_xchg_set_streams(pgx_xchg* x, void* const* streams, int n);
 int pgx_xchg_join(pgx_xchg* x, int layer, void* stream);
 /* Kernels this exchange object has launched so far (exchange + gate kernels). */
 int pgx_xchg_launch_count(pgx_xchg* x, uint64_t* count_out);
+/* Whole-model gate: one launch waiting for every layer's arrivals of `iteration`
+ * (same relative convention as pgx_xchg_gate in device-iteration mode). */
+int pgx_xchg_gate_all(pgx_xchg* x, uint32_t iteration, void* stream);
 /* Per-layer launch statistics for the roofline (bytes moved per launch). */
 int pgx_xchg_layer_bytes(pgx_xchg* x, int layer, uint64_t* nvlink_out_bytes,
                          uint64_t* hbm_bytes);

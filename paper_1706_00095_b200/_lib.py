@@ -87,6 +87,7 @@ SIGNATURES = {
     "pgx_xchg_connect": [vp],
     "pgx_xchg_layer": [vp, i32, u32, P(vp), P(u64), i32, i32, vp],
     "pgx_xchg_gate": [vp, i32, u32, vp],
+    "pgx_xchg_gate_all": [vp, u32, vp],
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],

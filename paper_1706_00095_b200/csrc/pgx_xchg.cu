@@ -467,6 +467,18 @@ __global__ void k_signal(FlagOut fo, uint32_t value, const uint32_t* iter) {
 
 __global__ void k_tick(uint32_t* iter) { *iter += 1; }
 
+// Whole-model gate: every (flag, multiplier) entry of every layer in one launch;
+// entry i waits until *flag >= it * mult, it = the awaited iteration + 1.
+struct GateEntry {
+  const uint32_t* flag;
+  uint32_t mult;
+};
+__global__ void k_gate_all(const GateEntry* __restrict__ ents, int n, uint32_t it_host, const uint32_t* iter,
+                           uint32_t add, Status st) {
+  const uint32_t it = iter ? *iter + add : it_host;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) wait_geq(ents[i].flag, it * ents[i].mult, st);
+}
+
 template <int N, class T>
 __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
   constexpr int W = VecT<T>::W;
@@ -565,6 +577,8 @@ struct pgx_xchg {
   uint32_t* iter_dev = nullptr;                    // device iteration counter (graph mode)
   bool device_iter = false;
   uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
+  GateEntry* gate_table = nullptr;                 // device: every layer's arrival flags
+  int gate_entries = 0;
 };
 
 namespace {
@@ -884,6 +898,27 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       return fail(PGX_E_CUDA, "exchange allocation failed: %s", cudaGetErrorString(e));
     }
   }
+  {  // whole-model gate table (all arrival flags live in this rank's own model segment)
+    std::vector<GateEntry> ents;
+    for (int l = 0; l < cfg->num_layers; ++l) {
+      const LayerPlan& P = x->L[l];
+      if (P.variant == PGX_VARIANT_TWOSHOT_CE) {
+        for (int j = 0; j < N; ++j)
+          if (j != x->rank) ents.push_back({x->mflags + x->ownerflag_base + (uint64_t)l * N + j, 1u});
+      } else if (P.expected) {
+        ents.push_back({x->mflags + l, P.expected});
+      }
+    }
+    x->gate_entries = (int)ents.size();
+    int prev;
+    cudaGetDevice(&prev);
+    cudaSetDevice(x->dev);
+    cudaError_t e = cudaMalloc(&x->gate_table, std::max<size_t>(1, ents.size()) * sizeof(GateEntry));
+    if (e == cudaSuccess && !ents.empty())
+      e = cudaMemcpy(x->gate_table, ents.data(), ents.size() * sizeof(GateEntry), cudaMemcpyHostToDevice);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return fail(PGX_E_CUDA, "gate table: %s", cudaGetErrorString(e));
+  }
   *out = x;
   return PGX_OK;
 }
@@ -904,6 +939,7 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   for (auto& v : x->part_ev)
     for (auto& e : v) cudaEventDestroy(e.e);
   if (x->iter_dev) cudaFree(x->iter_dev);
+  if (x->gate_table) cudaFree(x->gate_table);
   if (x->own_streams) {
     if (x->down) cudaStreamDestroy(x->down);
     if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
@@ -1112,6 +1148,29 @@ int pgx_xchg_join(pgx_xchg* x, int l, void* stream) {
 
 int pgx_xchg_launch_count(pgx_xchg* x, uint64_t* n) {
   *n = x->launches;
+  return PGX_OK;
+}
+
+int pgx_xchg_gate_all(pgx_xchg* x, uint32_t iteration, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  int prev;
+  cudaGetDevice(&prev);
+  if (prev != x->dev) cudaSetDevice(x->dev);
+  cudaError_t e = cudaSuccess;
+  for (size_t l = 0; l < x->L.size() && e == cudaSuccess; ++l) {
+    e = xwait(s, x->done[l]);
+    if (e == cudaSuccess) e = xwait(s, x->rs_done[l]);
+    if (e == cudaSuccess) e = xwait(s, x->rs2_done[l]);
+    if (e == cudaSuccess) e = xwait(s, x->down_done[l]);
+  }
+  if (e == cudaSuccess && x->gate_entries) {
+    ++x->launches;
+    k_gate_all<<<1, 256, 0, s>>>(x->gate_table, x->gate_entries, iteration + 1,
+                                  x->device_iter ? x->iter_dev : nullptr, iteration + 1, world_status(x->w));
+    e = cudaGetLastError();
+  }
+  if (prev != x->dev) cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "gate_all failed: %s", cudaGetErrorString(e));
   return PGX_OK;
 }
 

@@ -143,6 +143,11 @@ class DeviceExchange:
         s = stream if stream is not None else torch.cuda.current_stream(self.tr.device)
         _lib.call("pgx_xchg_tick", self.handle, s.cuda_stream)
 
+    def gate_all(self, iteration: int, stream=None) -> None:
+        """One launch gating `stream` on every layer's arrivals of `iteration`."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.tr.device)
+        _lib.call("pgx_xchg_gate_all", self.handle, iteration & 0xFFFFFFFF, s.cuda_stream)
+
     def join(self, layer: int, stream) -> None:
         """Make `stream` wait until this rank's part of layer's last exchange is done."""
         _lib.call("pgx_xchg_join", self.handle, layer, stream.cuda_stream)
@@ -176,7 +181,15 @@ class ModuleBinding:
     forward-pre-hook gates on the previous iteration's exchange of that layer.
     """
 
-    def __init__(self, xchg: DeviceExchange, layers):
+    def __init__(self, xchg: DeviceExchange, layers, gate: str = "layer"):
+        """gate="layer": each module's forward waits for its own layer (finest overlap);
+        gate="model": the first forward hook of a step waits for all layers in ONE launch
+        (fewer launches for many-small-layer nets; in CNNs the first layer is also the
+        last one exchanged, so little overlap is lost)."""
+        if gate not in ("layer", "model"):
+            raise ConfigError(f"gate must be 'layer' or 'model', got {gate!r}")
+        self.gate_mode = gate
+        self._gated_step = None
         self.x = xchg
         self.layers = layers
         self.k = 0
@@ -245,6 +258,17 @@ class ModuleBinding:
 
     def _make_gate(self, l):
         def pre_hook(_mod, _inp):
+            if self.gate_mode == "model":
+                if self._gated_step == self.k:
+                    return
+                self._gated_step = self.k
+                if self.x.device_iteration:
+                    self.x.gate_all(-1)
+                    self.gpu_launches += 1
+                elif self.k > 0:
+                    self.x.gate_all(self.k - 1)
+                    self.gpu_launches += 1
+                return
             if self.x.device_iteration:
                 self.x.gate(l, -1)  # relative: the previous iteration
                 self.gpu_launches += 1

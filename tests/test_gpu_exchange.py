@@ -172,7 +172,8 @@ class _FixedGrad(torch.nn.Module):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce"])
-def test_cuda_graph_replay_matches_oracle(cuda, variant):
+@pytest.mark.parametrize("gate", ["layer", "model"])
+def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     """A captured training step (device iteration counter) applies exactly the oracle update."""
     from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
     from paper_1706_00095_b200.transport import LocalWorld
@@ -185,7 +186,7 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant):
     x.connect()
     w = torch.cat([m.weight.detach(), m.bias.detach()]).cpu().numpy()
     g = torch.cat([m.c, m.d]).cpu().numpy()
-    bind = ModuleBinding(x, layers)
+    bind = ModuleBinding(x, layers, gate=gate)
     v = np.zeros_like(w)
 
     def step():

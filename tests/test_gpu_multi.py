@@ -181,7 +181,7 @@ def _cifar10_quick():
     return Quick()
 
 
-def _model_worker(rank, world, port, which, variant, q):
+def _model_worker(rank, world, port, which, variant, gate, q):
     """configs[0] / configs[1]: a real model trained through ModuleBinding; every step's
     exchanged weights must equal the oracle applied to the gradients the hooks saw."""
     import torch.distributed as dist
@@ -204,7 +204,7 @@ def _model_worker(rank, world, port, which, variant, q):
         tr = DistTransport(rank, world, rank, timeout_s=20.0)
         x = DeviceExchange(tr, [sum(p.numel() for p in ps) for _, ps in layers], mode="fast32", variant=variant,
                            **hyper)
-        bind = ModuleBinding(x, layers)
+        bind = ModuleBinding(x, layers, gate=gate)
         tr.barrier()
         x.connect()
         seen = {}
@@ -248,9 +248,10 @@ def _model_worker(rank, world, port, which, variant, q):
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("which", ["lenet", "cifar10_quick"])
-@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "tree"])
-def test_real_models_match_oracle(which, variant):
+@pytest.mark.parametrize("variant,gate", [("twoshot", "layer"), ("twoshot_ce", "layer"), ("tree", "layer"),
+                                          ("twoshot_ce", "model")])
+def test_real_models_match_oracle(which, variant, gate):
     world = 2 if which == "lenet" else min(4, _ngpu())
-    out = _spawn(_model_worker, world, which, variant)
+    out = _spawn(_model_worker, world, which, variant, gate)
     for rank, bad, status in out:
         assert bad == [] and status == 0, (rank, bad, status)
