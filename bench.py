@@ -424,23 +424,36 @@ def pgx_arm(args):
 
     nvl, hbm = xchg.layer_bytes(L_DOM)
     avg = statistics.mean(durs) if durs else None
+    kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local + copy-engine transfers",
+             "tree": "k_tree_up/k_tree_down"}[xchg.variants[L_DOM]]
+    what = "%s, layer %d (%d params): fold + fused momentum update%s" % (
+        kname, L_DOM, sizes[L_DOM], " + reduce-scatter/all-gather over NVLink" if world > 1 else "")
+    measured_in = (("CUDA events captured in the step graph, %d replays after the timed region" % len(durs))
+                   if graph is not None else "CUDA events in every timed eager step")
+    traffic = ncu_traffic(kname.split()[0], world, sizes[L_DOM])
     roof = None
-    if avg:
-        ach = hbm / (avg / 1e3) / 1e9
+    if avg and world == 1:  # one GPU: the fused update is an HBM stream
         peak, peak_src = hbm_peak()
-        kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local + copy-engine transfers",
-                 "tree": "k_tree_up/k_tree_down"}[xchg.variants[L_DOM]]
-        roof = {"bound": "hbm", "kernel": "%s (layer %d, %d params: fold + fused momentum update%s)" %
-                (kname, L_DOM, sizes[L_DOM], " + peer transfers" if world > 1 else ""), "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": None, "algorithmic_bytes_per_launch": hbm,
-                "avg_launch_ms_in_step": avg, "peak_source": peak_src,
-                "launch_share_of_step": avg / (ms / args.steps),
-                "measured_in": ("CUDA events captured in the step graph, %d replays after the timed region"
-                                % len(durs)) if graph is not None else "CUDA events in every timed eager step"}
-        if iso and world == 1:
+        ach = hbm / (avg / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": what, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": traffic, "algorithmic_bytes_per_launch": hbm, "avg_launch_ms_in_step": avg,
+                "peak_source": peak_src, "launch_share_of_step": avg / (ms / args.steps), "measured_in": measured_in}
+        if iso:
             roof["isolated_launch_ms"] = statistics.median(iso)
             roof["isolated_achieved"] = hbm / (statistics.median(iso) / 1e3) / 1e9
             roof["isolated_frac"] = roof["isolated_achieved"] / peak
+    elif avg:  # several GPUs: the layer's exchange is bound by this GPU's NVLink out-bandwidth
+        iso_ms = statistics.median(iso)
+        ach = nvl / (avg / 1e3) / 1e9
+        roof = {"bound": "nvlink", "kernel": what, "achieved": ach, "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                "frac": ach / NVLINK_PEAK_GBS, "traffic": traffic, "algorithmic_bytes_per_launch": nvl,
+                "bytes": "2(N-1)/N x layer bytes leave this GPU (reduce-scatter + all-gather)",
+                "avg_launch_ms_in_step": avg, "launch_share_of_step": avg / (ms / args.steps),
+                "peak_source": "B200_PROFILING.md measured NVLink peer copy per direction (900 nominal)",
+                "measured_in": measured_in + "; in-step time includes waiting for the slowest rank's gradient",
+                "isolated_ms": iso_ms, "isolated_achieved": nvl / (iso_ms / 1e3) / 1e9,
+                "isolated_frac": nvl / (iso_ms / 1e3) / 1e9 / NVLINK_PEAK_GBS,
+                "hbm_bytes_per_launch": hbm}
     line = {"metric": wl["metric"], "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
@@ -450,15 +463,6 @@ def pgx_arm(args):
         line["config"]["per_gpu_batch"] = B
         line["config"]["global_batch"] = gb
         line["config"]["diagnostic"] = "per-GPU batch overridden; not the headline configuration"
-    if world > 1 and avg:
-        iso_ms = statistics.median(iso)
-        line["roofline_nvlink"] = {"bound": "nvlink", "achieved": nvl / (avg / 1e3) / 1e9, "peak": NVLINK_PEAK_GBS,
-                                   "unit": "GB/s", "frac": nvl / (avg / 1e3) / 1e9 / NVLINK_PEAK_GBS,
-                                   "bytes_per_launch": nvl, "peak_source": "B200_PROFILING.md measured peer copy",
-                                   "what": "dominant layer's whole exchange (RS + fold/update + AG + arrival), "
-                                           "this rank's out-bytes over its in-step duration",
-                                   "isolated_ms": iso_ms, "isolated_achieved": nvl / (iso_ms / 1e3) / 1e9,
-                                   "isolated_frac": nvl / (iso_ms / 1e3) / 1e9 / NVLINK_PEAK_GBS}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_step_timing(world, seconds=args.cpu_seconds, workload=args.workload)
     if rank == 0:
@@ -606,6 +610,18 @@ def comparison_arm(args):
                           "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
                           "impl": "comparison-" + args.variant}), flush=True)
     dist.destroy_process_group()
+
+
+def ncu_traffic(kernel: str, world: int, layer_params: int):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/ncu_traffic.json), when one exists for this kernel/world/layer; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            table = json.load(fh)
+    except Exception:  # noqa: BLE001
+        return None
+    rec = table.get(f"{kernel}/N{world}/{layer_params}")
+    return None if rec is None else rec["dram_read_bytes"] + rec["dram_write_bytes"]
 
 
 def hbm_peak():
