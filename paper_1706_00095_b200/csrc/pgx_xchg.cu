@@ -432,6 +432,134 @@ __global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
   retire(a.queue);
 }
 
+// ============================================================== TMA push
+// Reduce-scatter push through the Tensor Memory Accelerator: one thread per CTA moves a
+// chunk as bulk copies global -> shared (mbarrier complete_tx) -> peer global (bulk
+// group), so the SM's load/store pipes and registers stay free for the backward kernels
+// running beside it; the remote write path is the TMA unit's full-line bulk stores.
+constexpr int kTmaStage = 16384;  // bytes per smem stage
+constexpr int kTmaStages = 4;     // 64 KB = one default chunk in flight per CTA
+constexpr int kTmaThreads = 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Copy [src, src+bytes) -> dst by TMA, 16-byte granular; returns the bytes NOT copied
+// (a <16-byte tail or misaligned range is left to the caller).  Caller: one thread.
+__device__ __forceinline__ uint64_t tma_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes, uint8_t* stages,
+                                             uint64_t* bars, uint32_t& phase) {
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return bytes;
+  uint64_t body = bytes & ~uint64_t(15), off = 0;
+  while (off < body) {
+    int used = 0;
+    for (; used < kTmaStages && off + (uint64_t)used * kTmaStage < body; ++used) {
+      uint64_t o = off + (uint64_t)used * kTmaStage;
+      uint32_t n = (uint32_t)min((uint64_t)kTmaStage, body - o);
+      mbar_expect_tx(&bars[used], n);
+      tma_load(stages + used * kTmaStage, src + o, n, &bars[used]);
+    }
+    for (int k = 0; k < used; ++k) {
+      uint64_t o = off + (uint64_t)k * kTmaStage;
+      uint32_t n = (uint32_t)min((uint64_t)kTmaStage, body - o);
+      mbar_wait(&bars[k], phase);
+      tma_store(dst + o, stages + k * kTmaStage, n);
+      tma_commit();
+    }
+    phase ^= 1u;
+    off += (uint64_t)used * kTmaStage;
+    tma_wait_all();  // stores finished (also frees the stages for the next round)
+  }
+  return bytes - body;
+}
+
+__global__ void __launch_bounds__(kTmaThreads) k_push_tma(XArgs a) {
+  extern __shared__ __align__(128) uint8_t tma_smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tma_smem + kTmaStages * kTmaStage);
+  __shared__ uint32_t s_item;
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  const int me = a.rank, N = a.world;
+  const int esz = a.mode == PGX_MODE_REF64 ? 8 : 4;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;
+  while (true) {
+    if (threadIdx.x == 0) s_item = atomicAdd(a.queue, 1u) + a.item_begin;
+    __syncwarp();
+    uint32_t it = s_item;
+    __syncwarp();
+    if (it >= a.item_end) break;
+    uint32_t c = it / (uint32_t)(N - 1);
+    int j = it % (N - 1);
+    j += (j >= me);
+    uint64_t lo = j * a.sl + (uint64_t)c * a.CH;
+    uint64_t hi = min(min(lo + a.CH, (uint64_t)(j + 1) * a.sl), a.S);
+    if (lo >= hi) continue;
+    uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + (lo - j * a.sl)) * esz;
+    if (threadIdx.x == 0) {
+      uint64_t pb = 0;
+      for (int k = 0; k < a.g.n; ++k) {  // the chunk may straddle gradient pieces (dW | db)
+        uint64_t pe = a.g.end[k], ol = max(lo, pb), oh = min(hi, pe);
+        if (ol < oh) {
+          const uint8_t* src = static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz;
+          uint8_t* d = dst + (ol - lo) * esz;
+          uint64_t bytes = (oh - ol) * esz;
+          uint64_t rest = tma_copy(d, src, bytes, tma_smem, bars, phase);
+          for (uint64_t b = bytes - rest; b < bytes; ++b) d[b] = src[b];  // ragged tail / misaligned
+        }
+        pb = pe;
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy writes before the flag
+      fence_acq_rel_sys();
+      st_release_sys(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
+    }
+    __syncwarp();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t done = atomicAdd(a.queue + 1, 1u);
+    if (done == gridDim.x - 1) {
+      a.queue[0] = 0;
+      a.queue[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
 // Gate: the stream proceeds once `want` chunk arrivals were counted.
 // want = *iter * per_epoch (graph mode: gate for the iteration before the current one)
 __global__ void k_gate(const uint32_t* counter, uint32_t want, const uint32_t* iter, uint32_t add, uint32_t per_epoch,
@@ -568,6 +696,7 @@ struct pgx_xchg {
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
   cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
+  bool tma_push = false;                           // TWOSHOT: reduce-scatter push via TMA bulk copies
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
@@ -874,6 +1003,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs2, cudaStreamNonBlocking, hi_prio);
     if (const char* v = getenv("PGX_CE_PARTS")) x->ce_parts = std::max(1, std::min(8, atoi(v)));
     if (const char* v = getenv("PGX_CE_RS_STREAMS")) x->ce_rs_streams = std::max(1, std::min(2, atoi(v)));
+    if (const char* v = getenv("PGX_TMA_PUSH")) x->tma_push = atoi(v) != 0;
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
     x->rs_done.resize(cfg->num_layers);
@@ -999,6 +1129,21 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     return rc;
   }
   xrecord(x->ready[l], s);
+  if (P.variant == PGX_VARIANT_TWOSHOT && x->tma_push && x->world > 1 && (phases & PGX_PHASE_PUSH)) {
+    // push through the TMA engine, then the owner phase on the same stream
+    a.item_begin = 0;
+    a.item_end = P.push_items;
+    static bool attr = false;
+    const int smem = kTmaStages * kTmaStage + kTmaStages * 8;
+    if (!attr) {
+      cudaFuncSetAttribute(k_push_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    int grid = (int)std::min<uint32_t>(P.push_items, (uint32_t)(3 * sm_count(x->dev)));
+    k_push_tma<<<grid, kTmaThreads, smem, s>>>(a);
+    ++x->launches;
+    phases &= ~PGX_PHASE_PUSH;
+  }
   if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
