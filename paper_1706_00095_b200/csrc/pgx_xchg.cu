@@ -1133,11 +1133,11 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     // push through the TMA engine, then the owner phase on the same stream
     a.item_begin = 0;
     a.item_end = P.push_items;
-    static bool attr = false;
+    static uint32_t attr_done = 0;  // per device: the attribute is a per-device function property
     const int smem = kTmaStages * kTmaStage + kTmaStages * 8;
-    if (!attr) {
+    if (!(attr_done & (1u << x->dev))) {
       cudaFuncSetAttribute(k_push_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
+      attr_done |= 1u << x->dev;
     }
     int grid = (int)std::min<uint32_t>(P.push_items, (uint32_t)(3 * sm_count(x->dev)));
     k_push_tma<<<grid, kTmaThreads, smem, s>>>(a);
