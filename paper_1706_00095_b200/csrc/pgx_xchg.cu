@@ -170,9 +170,11 @@ __device__ __forceinline__ void update_vec(T* w, const T* g, float* v, int cnt, 
 
 // Owner work on U vectors per thread: all loads first (U*(N+2) 16-byte requests in
 // flight), then tree-order fold, fused update, local + peer stores.
+// kRemote: store the updated vector into every peer's weights (register path);
+// tile != nullptr: also stage it in shared memory for TMA bulk stores.
 template <int N, class T, int U, bool kRemote = true>
 __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint64_t lo, uint64_t hi,
-                                              uint64_t q0, uint64_t nvec) {
+                                              uint64_t q0, uint64_t nvec, T* tile = nullptr) {
   constexpr int W = VecT<T>::W;
   const int me = a.rank;
   const bool fast = sizeof(T) == 4 && a.mode == PGX_MODE_FAST32;
@@ -215,6 +217,7 @@ __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint
     }
     st_vec<T>(static_cast<T*>(a.model[me]) + e, cnt[u], w[u]);
     if (fast) st_vec<float>(a.v + e, cnt[u], vv[u]);
+    if (tile) st_vec<T>(tile + (e - lo), cnt[u], w[u]);
     if constexpr (kRemote) {
 #pragma unroll
       for (int s = 0; s < N; ++s)
@@ -560,6 +563,80 @@ __global__ void __launch_bounds__(kTmaThreads) k_push_tma(XArgs a) {
   }
 }
 
+// Owner phase with a TMA all-gather: the CTA folds + updates a chunk into a shared-memory
+// tile, then one thread bulk-stores the tile into every peer's weights.
+template <int N, class T>
+__global__ void __launch_bounds__(kThreads) k_owner_tma(XArgs a) {
+  constexpr int W = VecT<T>::W;
+  extern __shared__ __align__(128) uint8_t tile_raw[];
+  T* tile = reinterpret_cast<T*>(tile_raw);
+  __shared__ uint32_t s_item;
+  __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  const int me = a.rank;
+  while (true) {
+    uint32_t it = claim(a.queue, &s_item) + a.item_begin;
+    if (it >= a.item_end) break;
+    uint32_t c = it - a.push_items;
+    uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
+    uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
+    if (lo >= hi) continue;
+    if (threadIdx.x < N - 1) {
+      int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
+      s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)s * a.C + c;
+    }
+    __syncthreads();
+    cta_wait_flags(s_flags, N - 1, epoch, a.st);
+    const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
+    uint64_t nvec = (hi - lo + W - 1) / W;
+    constexpr int U = N <= 4 ? 2 : 1;
+    for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
+      owner_vectors<N, T, U, false>(a, rxb, lo, hi, q0, nvec, tile);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+      const uint64_t bytes = (hi - lo) * sizeof(T), body = bytes & ~uint64_t(15);
+      for (int d = 1; d < N; ++d) {
+        uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + lo);
+        for (uint64_t o = 0; o < body; o += 65536) {
+          uint32_t n = (uint32_t)min((uint64_t)65536, body - o);
+          tma_store(dst + o, tile_raw + o, n);
+        }
+        tma_commit();
+      }
+      tma_wait_all();
+      for (int d = 1; d < N; ++d) {  // ragged tail of the layer
+        uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + lo);
+        for (uint64_t b = body; b < bytes; ++b) dst[b] = tile_raw[b];
+      }
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      fence_acq_rel_sys();
+      for (int d = 1; d < N; ++d) red_release_sys_add(a.mflags[(me + d) % N] + a.layer, 1u);
+    }
+    __syncthreads();
+  }
+  retire(a.queue);
+}
+
+template <class T>
+void launch_owner_tma(int N, int grid, size_t smem, cudaStream_t s, const XArgs& a, int dev) {
+  static uint32_t attr_done[PGX_MAX_RANKS + 1] = {};
+  switch (N) {
+#define PGX_CASE(n)                                                                          \
+  case n:                                                                                    \
+    if (!(attr_done[n] & (1u << dev))) {                                                     \
+      cudaFuncSetAttribute(k_owner_tma<n, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                           (int)smem);                                                       \
+      attr_done[n] |= 1u << dev;                                                             \
+    }                                                                                        \
+    k_owner_tma<n, T><<<grid, kThreads, smem, s>>>(a);                                       \
+    break;
+    PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
 // Gate: the stream proceeds once `want` chunk arrivals were counted.
 // want = *iter * per_epoch (graph mode: gate for the iteration before the current one)
 __global__ void k_gate(const uint32_t* counter, uint32_t want, const uint32_t* iter, uint32_t add, uint32_t per_epoch,
@@ -697,6 +774,7 @@ struct pgx_xchg {
   cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
   bool tma_push = false;                           // TWOSHOT: reduce-scatter push via TMA bulk copies
+  bool tma_ag = false;                             // TWOSHOT: all-gather via TMA bulk stores
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
@@ -1004,6 +1082,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (const char* v = getenv("PGX_CE_PARTS")) x->ce_parts = std::max(1, std::min(8, atoi(v)));
     if (const char* v = getenv("PGX_CE_RS_STREAMS")) x->ce_rs_streams = std::max(1, std::min(2, atoi(v)));
     if (const char* v = getenv("PGX_TMA_PUSH")) x->tma_push = atoi(v) != 0;
+    if (const char* v = getenv("PGX_TMA_AG")) x->tma_ag = atoi(v) != 0;
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
     x->rs_done.resize(cfg->num_layers);
@@ -1143,6 +1222,19 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     k_push_tma<<<grid, kTmaThreads, smem, s>>>(a);
     ++x->launches;
     phases &= ~PGX_PHASE_PUSH;
+  }
+  if (P.variant == PGX_VARIANT_TWOSHOT && x->tma_ag && x->world > 1 && !(phases & PGX_PHASE_PUSH) &&
+      (phases & PGX_PHASE_OWNER)) {
+    a.item_begin = P.push_items;
+    a.item_end = P.items;
+    size_t smem = (size_t)x->cfg.chunk_elems * x->esz;
+    int grid = (int)std::min<uint32_t>(P.items - P.push_items, (uint32_t)P.grid);
+    if (x->esz == 8)
+      launch_owner_tma<double>(x->world, grid, smem, s, a, x->dev);
+    else
+      launch_owner_tma<float>(x->world, grid, smem, s, a, x->dev);
+    ++x->launches;
+    phases &= ~PGX_PHASE_OWNER;
   }
   if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
