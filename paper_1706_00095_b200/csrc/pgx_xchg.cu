@@ -773,8 +773,8 @@ struct pgx_xchg {
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
   cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
-  bool tma_push = false;                           // TWOSHOT: reduce-scatter push via TMA bulk copies
-  bool tma_ag = false;                             // TWOSHOT: all-gather via TMA bulk stores
+  bool tma_push = true;                            // TWOSHOT: reduce-scatter push via TMA bulk copies (r1o: +28%)
+  bool tma_ag = true;                              // TWOSHOT: all-gather via TMA bulk stores (r1p: +11%)
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
