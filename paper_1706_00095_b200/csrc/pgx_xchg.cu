@@ -261,12 +261,93 @@ __device__ __forceinline__ void cta_wait_flags(uint32_t* const* flags, int n, ui
   __syncthreads();
 }
 
+// ============================================================== TMA helpers
+// Bulk copies through the Tensor Memory Accelerator: global -> shared (mbarrier
+// complete_tx) and shared -> (peer) global (bulk group).  One thread drives them, so a
+// chunk's remote writes are full-line bulk stores issued without the SM's LSU pipe.
+constexpr int kTmaStage = 16384;  // bytes per smem stage
+constexpr int kTmaStages = 4;     // 64 KB = one default chunk in flight per CTA
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Copy [src, src+bytes) -> dst by TMA, 16-byte granular; returns the bytes NOT copied
+// (a <16-byte tail or misaligned range is left to the caller).  Caller: one thread.
+__device__ __forceinline__ uint64_t tma_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes, uint8_t* stages,
+                                             uint64_t* bars, uint32_t& phase) {
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return bytes;
+  uint64_t body = bytes & ~uint64_t(15), off = 0;
+  while (off < body) {
+    int used = 0;
+    for (; used < kTmaStages && off + (uint64_t)used * kTmaStage < body; ++used) {
+      uint64_t o = off + (uint64_t)used * kTmaStage;
+      uint32_t n = (uint32_t)min((uint64_t)kTmaStage, body - o);
+      mbar_expect_tx(&bars[used], n);
+      tma_load(stages + used * kTmaStage, src + o, n, &bars[used]);
+    }
+    for (int k = 0; k < used; ++k) {
+      uint64_t o = off + (uint64_t)k * kTmaStage;
+      uint32_t n = (uint32_t)min((uint64_t)kTmaStage, body - o);
+      mbar_wait(&bars[k], phase);
+      tma_store(dst + o, stages + k * kTmaStage, n);
+      tma_commit();
+    }
+    phase ^= 1u;
+    off += (uint64_t)used * kTmaStage;
+    tma_wait_all();  // stores finished (also frees the stages for the next round)
+  }
+  return bytes - body;
+}
+
 // ============================================================== TWOSHOT
-template <int N, class T>
+// kTma (N > 1): push chunks and all-gather tiles move as TMA bulk copies through a
+// 64 KB shared-memory buffer (dynamic smem), driven by thread 0.
+template <int N, class T, bool kTma>
 __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
   constexpr int W = VecT<T>::W;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  extern __shared__ __align__(128) uint8_t tma_buf[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tma_buf + kTmaStages * kTmaStage);
+  uint32_t tma_phase = 0;
+  if constexpr (kTma) {
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+  }
 
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
@@ -282,7 +363,27 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
       j += (j >= me);
       uint64_t lo = j * a.sl + (uint64_t)c * a.CH;
       uint64_t hi = min(min(lo + a.CH, (uint64_t)(j + 1) * a.sl), a.S);
-      if (lo < hi) {
+      if (lo < hi && kTma) {
+        T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + (lo - j * a.sl));
+        if (threadIdx.x == 0) {
+          uint64_t pb = 0;
+          for (int k = 0; k < a.g.n; ++k) {  // the chunk may straddle gradient pieces (dW | db)
+            uint64_t pe = a.g.end[k], ol = max(lo, pb), oh = min(hi, pe);
+            if (ol < oh) {
+              const uint8_t* src = static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * sizeof(T);
+              uint8_t* d = reinterpret_cast<uint8_t*>(dst + (ol - lo));
+              uint64_t bytes = (oh - ol) * sizeof(T);
+              uint64_t rest = tma_copy(d, src, bytes, tma_buf, bars, tma_phase);
+              for (uint64_t b = bytes - rest; b < bytes; ++b) d[b] = src[b];  // ragged tail / misaligned
+            }
+            pb = pe;
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy writes before the flag
+          fence_acq_rel_sys();
+          st_release_sys(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
+        }
+        __syncthreads();
+      } else if (lo < hi) {
         T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + (lo - j * a.sl));
         uint64_t nvec = (hi - lo + W - 1) / W;
         constexpr int UP = 4;
@@ -317,13 +418,38 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
       const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
       uint64_t nvec = (hi - lo + W - 1) / W;
       constexpr int U = N <= 4 ? 2 : 1;
-      for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
-        owner_vectors<N, T, U>(a, rxb, lo, hi, q0, nvec);
-      __syncthreads();
-      if (threadIdx.x < N - 1) {
-        int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
-        fence_acq_rel_sys();
-        red_release_sys_add(a.mflags[s] + a.layer, 1u);
+      if constexpr (kTma) {
+        T* tile = reinterpret_cast<T*>(tma_buf);
+        for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
+          owner_vectors<N, T, U, false>(a, rxb, lo, hi, q0, nvec, tile);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+          const uint64_t bytes = (hi - lo) * sizeof(T), body = bytes & ~uint64_t(15);
+          for (int d = 1; d < N; ++d) {
+            uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + lo);
+            for (uint64_t o = 0; o < body; o += kTmaStage) tma_store(dst + o, tma_buf + o, (uint32_t)min((uint64_t)kTmaStage, body - o));
+            tma_commit();
+          }
+          tma_wait_all();
+          for (int d = 1; d < N; ++d) {  // ragged tail of the layer
+            uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + lo);
+            for (uint64_t b = body; b < bytes; ++b) dst[b] = tma_buf[b];
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          fence_acq_rel_sys();
+          for (int d = 1; d < N; ++d) red_release_sys_add(a.mflags[(me + d) % N] + a.layer, 1u);
+        }
+        __syncthreads();  // the tile is reused by the next item
+      } else {
+        for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
+          owner_vectors<N, T, U>(a, rxb, lo, hi, q0, nvec);
+        __syncthreads();
+        if (threadIdx.x < N - 1) {
+          int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
+          fence_acq_rel_sys();
+          red_release_sys_add(a.mflags[s] + a.layer, 1u);
+        }
       }
     }
   }
@@ -433,208 +559,6 @@ __global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
     }
   }
   retire(a.queue);
-}
-
-// ============================================================== TMA push
-// Reduce-scatter push through the Tensor Memory Accelerator: one thread per CTA moves a
-// chunk as bulk copies global -> shared (mbarrier complete_tx) -> peer global (bulk
-// group), so the SM's load/store pipes and registers stay free for the backward kernels
-// running beside it; the remote write path is the TMA unit's full-line bulk stores.
-constexpr int kTmaStage = 16384;  // bytes per smem stage
-constexpr int kTmaStages = 4;     // 64 KB = one default chunk in flight per CTA
-constexpr int kTmaThreads = 32;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(smem_dst)),
-               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tma_store(void* gdst, const void* smem_src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-// Copy [src, src+bytes) -> dst by TMA, 16-byte granular; returns the bytes NOT copied
-// (a <16-byte tail or misaligned range is left to the caller).  Caller: one thread.
-__device__ __forceinline__ uint64_t tma_copy(uint8_t* dst, const uint8_t* src, uint64_t bytes, uint8_t* stages,
-                                             uint64_t* bars, uint32_t& phase) {
-  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) return bytes;
-  uint64_t body = bytes & ~uint64_t(15), off = 0;
-  while (off < body) {
-    int used = 0;
-    for (; used < kTmaStages && off + (uint64_t)used * kTmaStage < body; ++used) {
-      uint64_t o = off + (uint64_t)used * kTmaStage;
-      uint32_t n = (uint32_t)min((uint64_t)kTmaStage, body - o);
-      mbar_expect_tx(&bars[used], n);
-      tma_load(stages + used * kTmaStage, src + o, n, &bars[used]);
-    }
-    for (int k = 0; k < used; ++k) {
-      uint64_t o = off + (uint64_t)k * kTmaStage;
-      uint32_t n = (uint32_t)min((uint64_t)kTmaStage, body - o);
-      mbar_wait(&bars[k], phase);
-      tma_store(dst + o, stages + k * kTmaStage, n);
-      tma_commit();
-    }
-    phase ^= 1u;
-    off += (uint64_t)used * kTmaStage;
-    tma_wait_all();  // stores finished (also frees the stages for the next round)
-  }
-  return bytes - body;
-}
-
-__global__ void __launch_bounds__(kTmaThreads) k_push_tma(XArgs a) {
-  extern __shared__ __align__(128) uint8_t tma_smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tma_smem + kTmaStages * kTmaStage);
-  __shared__ uint32_t s_item;
-  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
-  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
-  const int me = a.rank, N = a.world;
-  const int esz = a.mode == PGX_MODE_REF64 ? 8 : 4;
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < kTmaStages; ++k) mbar_init(&bars[k], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncwarp();
-  uint32_t phase = 0;
-  while (true) {
-    if (threadIdx.x == 0) s_item = atomicAdd(a.queue, 1u) + a.item_begin;
-    __syncwarp();
-    uint32_t it = s_item;
-    __syncwarp();
-    if (it >= a.item_end) break;
-    uint32_t c = it / (uint32_t)(N - 1);
-    int j = it % (N - 1);
-    j += (j >= me);
-    uint64_t lo = j * a.sl + (uint64_t)c * a.CH;
-    uint64_t hi = min(min(lo + a.CH, (uint64_t)(j + 1) * a.sl), a.S);
-    if (lo >= hi) continue;
-    uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + (lo - j * a.sl)) * esz;
-    if (threadIdx.x == 0) {
-      uint64_t pb = 0;
-      for (int k = 0; k < a.g.n; ++k) {  // the chunk may straddle gradient pieces (dW | db)
-        uint64_t pe = a.g.end[k], ol = max(lo, pb), oh = min(hi, pe);
-        if (ol < oh) {
-          const uint8_t* src = static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz;
-          uint8_t* d = dst + (ol - lo) * esz;
-          uint64_t bytes = (oh - ol) * esz;
-          uint64_t rest = tma_copy(d, src, bytes, tma_smem, bars, phase);
-          for (uint64_t b = bytes - rest; b < bytes; ++b) d[b] = src[b];  // ragged tail / misaligned
-        }
-        pb = pe;
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy writes before the flag
-      fence_acq_rel_sys();
-      st_release_sys(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
-    }
-    __syncwarp();
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    uint32_t done = atomicAdd(a.queue + 1, 1u);
-    if (done == gridDim.x - 1) {
-      a.queue[0] = 0;
-      a.queue[1] = 0;
-      __threadfence();
-    }
-  }
-}
-
-// Owner phase with a TMA all-gather: the CTA folds + updates a chunk into a shared-memory
-// tile, then one thread bulk-stores the tile into every peer's weights.
-template <int N, class T>
-__global__ void __launch_bounds__(kThreads) k_owner_tma(XArgs a) {
-  constexpr int W = VecT<T>::W;
-  extern __shared__ __align__(128) uint8_t tile_raw[];
-  T* tile = reinterpret_cast<T*>(tile_raw);
-  __shared__ uint32_t s_item;
-  __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
-  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
-  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
-  const int me = a.rank;
-  while (true) {
-    uint32_t it = claim(a.queue, &s_item) + a.item_begin;
-    if (it >= a.item_end) break;
-    uint32_t c = it - a.push_items;
-    uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
-    uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
-    if (lo >= hi) continue;
-    if (threadIdx.x < N - 1) {
-      int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
-      s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)s * a.C + c;
-    }
-    __syncthreads();
-    cta_wait_flags(s_flags, N - 1, epoch, a.st);
-    const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
-    uint64_t nvec = (hi - lo + W - 1) / W;
-    constexpr int U = N <= 4 ? 2 : 1;
-    for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
-      owner_vectors<N, T, U, false>(a, rxb, lo, hi, q0, nvec, tile);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
-      const uint64_t bytes = (hi - lo) * sizeof(T), body = bytes & ~uint64_t(15);
-      for (int d = 1; d < N; ++d) {
-        uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + lo);
-        for (uint64_t o = 0; o < body; o += 65536) {
-          uint32_t n = (uint32_t)min((uint64_t)65536, body - o);
-          tma_store(dst + o, tile_raw + o, n);
-        }
-        tma_commit();
-      }
-      tma_wait_all();
-      for (int d = 1; d < N; ++d) {  // ragged tail of the layer
-        uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + lo);
-        for (uint64_t b = body; b < bytes; ++b) dst[b] = tile_raw[b];
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      fence_acq_rel_sys();
-      for (int d = 1; d < N; ++d) red_release_sys_add(a.mflags[(me + d) % N] + a.layer, 1u);
-    }
-    __syncthreads();
-  }
-  retire(a.queue);
-}
-
-template <class T>
-void launch_owner_tma(int N, int grid, size_t smem, cudaStream_t s, const XArgs& a, int dev) {
-  static uint32_t attr_done[PGX_MAX_RANKS + 1] = {};
-  switch (N) {
-#define PGX_CASE(n)                                                                          \
-  case n:                                                                                    \
-    if (!(attr_done[n] & (1u << dev))) {                                                     \
-      cudaFuncSetAttribute(k_owner_tma<n, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                           (int)smem);                                                       \
-      attr_done[n] |= 1u << dev;                                                             \
-    }                                                                                        \
-    k_owner_tma<n, T><<<grid, kThreads, smem, s>>>(a);                                       \
-    break;
-    PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
-#undef PGX_CASE
-  }
 }
 
 // Gate: the stream proceeds once `want` chunk arrivals were counted.
@@ -773,8 +697,7 @@ struct pgx_xchg {
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
   cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
-  bool tma_push = true;                            // TWOSHOT: reduce-scatter push via TMA bulk copies (r1o: +28%)
-  bool tma_ag = true;                              // TWOSHOT: all-gather via TMA bulk stores (r1p: +11%)
+  bool tma = true;                                 // TWOSHOT: push / all-gather as TMA bulk copies
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
@@ -834,26 +757,33 @@ XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
 
 // Grid = min(requested, resident CTAs): CTAs beyond what fits only spin up to
 // find the queue empty.
-template <int N, class T>
+constexpr size_t kTmaSmem = (size_t)kTmaStages * kTmaStage + kTmaStages * sizeof(uint64_t);
+
+template <int N, class T, bool kTma>
 int resident_grid(int want, int dev) {
-  static int cap = 0;  // per instantiation; one device model per process
-  if (!cap) {
+  static int cap[PGX_MAX_RANKS] = {};  // per instantiation and device
+  if (!cap[dev]) {
+    if (kTma) cudaFuncSetAttribute(k_twoshot<N, T, kTma>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_twoshot<N, T>, kThreads, 0);
-    cap = std::max(1, per_sm) * sm_count(dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_twoshot<N, T, kTma>, kThreads, kTma ? kTmaSmem : 0);
+    cap[dev] = std::max(1, per_sm) * sm_count(dev);
   }
-  return std::max(1, std::min(want, cap));
+  return std::max(1, std::min(want, cap[dev]));
 }
 
 template <class T>
-void launch_twoshot(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
+void launch_twoshot(int N, bool tma, int want, int dev, cudaStream_t s, const XArgs& a) {
   switch (N) {
-#define PGX_CASE(n)                                                    \
-  case n: {                                                            \
-    int g = resident_grid<n, T>(want, dev);                            \
-    k_twoshot<n, T><<<g, kThreads, 0, s>>>(a);                         \
-    break;                                                             \
-  }
+#define PGX_CASE(n)                                                                 \
+  case n:                                                                           \
+    if (n > 1 && tma) {                                                             \
+      int g = resident_grid<n, T, true>(want, dev);                                 \
+      k_twoshot<n, T, true><<<g, kThreads, kTmaSmem, s>>>(a);                       \
+    } else {                                                                        \
+      int g = resident_grid<n, T, false>(want, dev);                                \
+      k_twoshot<n, T, false><<<g, kThreads, 0, s>>>(a);                             \
+    }                                                                               \
+    break;
     PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
 #undef PGX_CASE
   }
@@ -1081,8 +1011,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs2, cudaStreamNonBlocking, hi_prio);
     if (const char* v = getenv("PGX_CE_PARTS")) x->ce_parts = std::max(1, std::min(8, atoi(v)));
     if (const char* v = getenv("PGX_CE_RS_STREAMS")) x->ce_rs_streams = std::max(1, std::min(2, atoi(v)));
-    if (const char* v = getenv("PGX_TMA_PUSH")) x->tma_push = atoi(v) != 0;
-    if (const char* v = getenv("PGX_TMA_AG")) x->tma_ag = atoi(v) != 0;
+    if (const char* v = getenv("PGX_TMA")) x->tma = atoi(v) != 0;
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
     x->rs_done.resize(cfg->num_layers);
@@ -1208,34 +1137,6 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     return rc;
   }
   xrecord(x->ready[l], s);
-  if (P.variant == PGX_VARIANT_TWOSHOT && x->tma_push && x->world > 1 && (phases & PGX_PHASE_PUSH)) {
-    // push through the TMA engine, then the owner phase on the same stream
-    a.item_begin = 0;
-    a.item_end = P.push_items;
-    static uint32_t attr_done = 0;  // per device: the attribute is a per-device function property
-    const int smem = kTmaStages * kTmaStage + kTmaStages * 8;
-    if (!(attr_done & (1u << x->dev))) {
-      cudaFuncSetAttribute(k_push_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr_done |= 1u << x->dev;
-    }
-    int grid = (int)std::min<uint32_t>(P.push_items, (uint32_t)(3 * sm_count(x->dev)));
-    k_push_tma<<<grid, kTmaThreads, smem, s>>>(a);
-    ++x->launches;
-    phases &= ~PGX_PHASE_PUSH;
-  }
-  if (P.variant == PGX_VARIANT_TWOSHOT && x->tma_ag && x->world > 1 && !(phases & PGX_PHASE_PUSH) &&
-      (phases & PGX_PHASE_OWNER)) {
-    a.item_begin = P.push_items;
-    a.item_end = P.items;
-    size_t smem = (size_t)x->cfg.chunk_elems * x->esz;
-    int grid = (int)std::min<uint32_t>(P.items - P.push_items, (uint32_t)P.grid);
-    if (x->esz == 8)
-      launch_owner_tma<double>(x->world, grid, smem, s, a, x->dev);
-    else
-      launch_owner_tma<float>(x->world, grid, smem, s, a, x->dev);
-    ++x->launches;
-    phases &= ~PGX_PHASE_OWNER;
-  }
   if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
@@ -1244,9 +1145,9 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
       ++x->launches;
       int grid = (int)std::min<uint32_t>(n, (uint32_t)P.grid);
       if (x->esz == 8)
-        launch_twoshot<double>(x->world, grid, x->dev, s, a);
+        launch_twoshot<double>(x->world, x->tma, grid, x->dev, s, a);
       else
-        launch_twoshot<float>(x->world, grid, x->dev, s, a);
+        launch_twoshot<float>(x->world, x->tma, grid, x->dev, s, a);
     }
   } else {
     if (phases & PGX_PHASE_PUSH) {
