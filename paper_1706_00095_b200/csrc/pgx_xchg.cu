@@ -697,7 +697,7 @@ struct pgx_xchg {
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
   cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
-  bool tma = true;                                 // TWOSHOT: push / all-gather as TMA bulk copies
+  bool tma = false;  // TWOSHOT: push / all-gather as TMA bulk copies (PGX_TMA=1; slower fused at N=4, profiles/r1r)
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
