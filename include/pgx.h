@@ -163,7 +163,9 @@ int pgx_seeded_fill_f32(uint64_t seed, double scale, float* out, uint64_t n, voi
 enum pgx_variant {
   PGX_VARIANT_TREE = 0,       /* paper: binomial reduce + master update + broadcast     */
   PGX_VARIANT_TWOSHOT = 1,    /* SM peer stores: reduce-scatter, owner update, gather   */
-  PGX_VARIANT_TWOSHOT_CE = 2  /* same schedule, shards moved by the copy engines        */
+  PGX_VARIANT_TWOSHOT_CE = 2, /* same schedule, shards moved by the copy engines        */
+  PGX_VARIANT_NVLS = 3        /* NVLink SHARP: in-switch reduce (multimem.ld_reduce) +
+                                 multicast weight store; fast32 only, tolerance parity  */
 };
 
 typedef struct pgx_xchg_config {
@@ -224,6 +226,14 @@ int pgx_xchg_set_streams(pgx_xchg* x, void* const* streams, int n);
 int pgx_xchg_join(pgx_xchg* x, int layer, void* stream);
 /* Kernels this exchange object has launched so far (exchange + gate kernels). */
 int pgx_xchg_launch_count(pgx_xchg* x, uint64_t* count_out);
+/* NVLS setup, collective over the ranks (after pgx_xchg_create, before use):
+ * rank 0 creates the multicast object and exports it as a POSIX fd (others get -1);
+ * the caller passes that fd to every other rank (SCM_RIGHTS); every rank imports it
+ * and adds its GPU; after ALL ranks added, every rank binds its local memory.  The
+ * weights then live in the multicast-backed buffer (re-query pgx_xchg_model). */
+int pgx_xchg_nvls_export(pgx_xchg* x, int* fd_out);
+int pgx_xchg_nvls_import(pgx_xchg* x, int fd);
+int pgx_xchg_nvls_bind(pgx_xchg* x);
 /* Whole-model gate: one launch waiting for every layer's arrivals of `iteration`
  * (same relative convention as pgx_xchg_gate in device-iteration mode). */
 int pgx_xchg_gate_all(pgx_xchg* x, uint32_t iteration, void* stream);

@@ -24,7 +24,7 @@ MAX_PIECES = 4
 XCHG_STREAMS = 5
 
 MODE_REF64, MODE_REF32, MODE_FAST32 = 0, 1, 2
-VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE = 0, 1, 2
+VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE, VARIANT_NVLS = 0, 1, 2, 3
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p
@@ -88,6 +88,9 @@ SIGNATURES = {
     "pgx_xchg_layer": [vp, i32, u32, P(vp), P(u64), i32, i32, vp],
     "pgx_xchg_gate": [vp, i32, u32, vp],
     "pgx_xchg_gate_all": [vp, u32, vp],
+    "pgx_xchg_nvls_export": [vp, P(i32)],
+    "pgx_xchg_nvls_import": [vp, i32],
+    "pgx_xchg_nvls_bind": [vp],
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],

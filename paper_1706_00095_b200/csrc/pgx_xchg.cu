@@ -20,8 +20,10 @@
 // into chunks (the notification unit, runtime.py:209-222) claimed through a
 // per-layer atomic queue: every non-waiting push chunk is claimed before any
 // waiting chunk, so a launch makes progress with any number of resident CTAs.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <vector>
 
@@ -561,6 +563,129 @@ __global__ void __launch_bounds__(kThreads) k_tree_down(XArgs a) {
   retire(a.queue);
 }
 
+// ============================================================== NVLS
+// NVLink SHARP: the switch reduces and multicasts.  Every rank publishes its layer
+// gradient into its slice of a multicast object; the owner of shard j reads the SUM of
+// all ranks' slices with one multimem.ld_reduce per vector (the reduction happens in the
+// NVSwitch), applies the fused update, and writes the new weights to every GPU with one
+// multimem.st.  Per GPU ~S bytes leave over NVLink instead of 2(N-1)/N*S.  The switch's
+// summation order is not the binomial order, so this variant is tolerance-only (fast32).
+struct NvArgs {
+  Pieces g;
+  float* uc_model;            // layer base, local mapping
+  float* uc_grad;             // layer base, local mapping
+  uint64_t mc_model, mc_grad; // layer base, multicast mapping
+  uint32_t* uc_ready;         // this layer's "all ranks published" counter (local view)
+  uint64_t mc_ready, mc_arrive;
+  uint32_t* pub_count;        // local: publish chunks completed (monotonic)
+  float* v;
+  uint32_t* queue;
+  uint64_t S, sl, CH;
+  uint32_t pub_items, items, epoch;
+  const uint32_t* iter;
+  int rank, world;
+  double lr;
+  float scale, mu, wd;
+  Status st;
+};
+
+__device__ __forceinline__ float4 mm_ld_reduce4(uint64_t addr) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(addr)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ float mm_ld_reduce1(uint64_t addr) {
+  float r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=f"(r) : "l"(addr) : "memory");
+  return r;
+}
+__device__ __forceinline__ void mm_st4(uint64_t addr, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mm_st1(uint64_t addr, float v) {
+  asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void mm_red_release_add(uint64_t addr, uint32_t v) {
+  asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ float fast32_update(float w, float g, float& v, const NvArgs& a) {
+  float gg = __fadd_rn(__fmul_rn(a.scale, g), __fmul_rn(a.wd, w));
+  float vv = __fadd_rn(__fmul_rn(a.mu, v), __fmul_rn((float)a.lr, gg));
+  v = vv;
+  return __fsub_rn(w, vv);
+}
+
+__global__ void __launch_bounds__(kThreads) k_nvls(NvArgs a) {
+  __shared__ uint32_t s_item;
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int me = a.rank;
+  const uint32_t pub_chunks = a.pub_items;
+  while (true) {
+    uint32_t it = claim(a.queue, &s_item);
+    if (it >= a.items) break;
+    if (it < a.pub_items) {
+      // ---- publish: this chunk of my gradient into my slice of the multicast object
+      uint64_t lo = (uint64_t)it * a.CH, hi = min(lo + a.CH, a.S);
+      for (uint64_t e = lo + threadIdx.x * 4; e < hi; e += (uint64_t)blockDim.x * 4) {
+        int cnt = (int)min((uint64_t)4, hi - e);
+        float buf[4];
+        grad_vec<float>(a.g, e, cnt, buf);
+        st_vec<float>(a.uc_grad + e, cnt, buf);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_acq_rel_sys();
+        uint32_t done = atomicAdd(a.pub_count, 1u) + 1;
+        if (done == pub_chunks) {  // my whole layer is published (the next launch is stream-ordered)
+          *a.pub_count = 0;
+          mm_red_release_add(a.mc_ready, 1u);
+        }
+      }
+    } else {
+      // ---- owner chunk: switch-reduced gradient, fused update, multicast store of the weights
+      uint32_t c = it - a.pub_items;
+      uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
+      uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
+      if (lo >= hi) continue;
+      if (threadIdx.x == 0) wait_geq(a.uc_ready, epoch * (uint32_t)a.world, a.st);
+      __syncthreads();
+      for (uint64_t e = lo + threadIdx.x * 4; e < hi; e += (uint64_t)blockDim.x * 4) {
+        if (e + 4 <= hi) {
+          float4 g = mm_ld_reduce4(a.mc_grad + e * 4);
+          float4 w = __ldcg(reinterpret_cast<const float4*>(a.uc_model + e));
+          float4 v = *reinterpret_cast<const float4*>(a.v + e);
+          w.x = fast32_update(w.x, g.x, v.x, a);
+          w.y = fast32_update(w.y, g.y, v.y, a);
+          w.z = fast32_update(w.z, g.z, v.z, a);
+          w.w = fast32_update(w.w, g.w, v.w, a);
+          *reinterpret_cast<float4*>(a.v + e) = v;
+          mm_st4(a.mc_model + e * 4, w);
+        } else {
+          for (uint64_t k = e; k < hi; ++k) {
+            float g = mm_ld_reduce1(a.mc_grad + k * 4);
+            float w = __ldcg(a.uc_model + k), v = a.v[k];
+            w = fast32_update(w, g, v, a);
+            a.v[k] = v;
+            mm_st1(a.mc_model + k * 4, w);
+          }
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_acq_rel_sys();
+        mm_red_release_add(a.mc_arrive, 1u);
+      }
+    }
+  }
+  retire(a.queue);
+}
+
 // Gate: the stream proceeds once `want` chunk arrivals were counted.
 // want = *iter * per_epoch (graph mode: gate for the iteration before the current one)
 __global__ void k_gate(const uint32_t* counter, uint32_t want, const uint32_t* iter, uint32_t add, uint32_t per_epoch,
@@ -709,6 +834,14 @@ struct pgx_xchg {
   uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
   GateEntry* gate_table = nullptr;                 // device: every layer's arrival flags
   int gate_entries = 0;
+  struct Nvls {                                    // NVLS: one multicast object [model | grad | flags]
+    bool on = false;
+    size_t size = 0;
+    CUmemGenericAllocationHandle mc = 0, mem = 0;
+    CUdeviceptr uc = 0, mcp = 0;                   // unicast (local) and multicast mappings
+    uint64_t grad_off = 0, flag_off = 0;           // bytes
+    uint32_t* pub_count = nullptr;                 // local per-layer publish-completion counters
+  } nv;
 };
 
 namespace {
@@ -800,6 +933,201 @@ void launch_owner_local(int N, int grid, cudaStream_t s, const XArgs& a) {
 }
 
 }  // namespace
+
+
+// ---------------------------------------------------------------- NVLS setup
+// Driver entry points through the runtime (libpgx.so does not link libcuda).
+template <class F>
+static F drv(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+#define PGX_DRV(fn) static auto p_##fn = drv<decltype(&fn)>(#fn)
+#define PGX_CU(call)                                                                      \
+  do {                                                                                    \
+    CUresult r__ = (call);                                                                \
+    if (r__ != CUDA_SUCCESS) return fail(PGX_E_CUDA, "%s failed (CUresult %d)", #call, (int)r__); \
+  } while (0)
+
+static bool nvls_layers(const pgx_xchg* x) {
+  for (auto& P : x->L)
+    if (P.variant == PGX_VARIANT_NVLS) return true;
+  return false;
+}
+
+static size_t nvls_size(pgx_xchg* x, size_t gran) {
+  uint64_t model_bytes = 0;
+  for (auto& P : x->L) model_bytes = std::max<uint64_t>(model_bytes, (P.model_off + P.S) * 4);
+  model_bytes = (model_bytes + 255) / 256 * 256;
+  x->nv.grad_off = model_bytes;
+  x->nv.flag_off = 2 * model_bytes;
+  size_t total = 2 * model_bytes + x->L.size() * 256;
+  return (total + gran - 1) / gran * gran;
+}
+
+static int nvls_granularity(pgx_xchg* x, size_t* gran) {
+  PGX_DRV(cuMulticastGetGranularity);
+  PGX_DRV(cuMemGetAllocationGranularity);
+  if (!p_cuMulticastGetGranularity || !p_cuMemGetAllocationGranularity)
+    return fail(PGX_E_CUDA, "multicast driver entry points unavailable");
+  CUmulticastObjectProp mp{};
+  mp.numDevices = x->world;
+  mp.size = 1 << 21;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g1 = 0, g2 = 0;
+  PGX_CU(p_cuMulticastGetGranularity(&g1, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = x->dev;
+  PGX_CU(p_cuMemGetAllocationGranularity(&g2, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  *gran = std::max(g1, g2);
+  return PGX_OK;
+}
+
+extern "C" int pgx_xchg_nvls_export(pgx_xchg* x, int* fd_out) {
+  *fd_out = -1;
+  if (!nvls_layers(x)) return fail(PGX_E_CONFIG, "no NVLS layers in this exchange");
+  if (x->cfg.mode != PGX_MODE_FAST32) return fail(PGX_E_CONFIG, "NVLS reduces in the switch: fast32 only");
+  size_t gran = 0;
+  int rc = nvls_granularity(x, &gran);
+  if (rc) return rc;
+  x->nv.size = nvls_size(x, gran);
+  if (x->rank != 0) return PGX_OK;
+  PGX_DRV(cuMulticastCreate);
+  PGX_DRV(cuMemExportToShareableHandle);
+  if (!p_cuMulticastCreate || !p_cuMemExportToShareableHandle) return fail(PGX_E_CUDA, "multicast entry points");
+  CUmulticastObjectProp mp{};
+  mp.numDevices = x->world;
+  mp.size = x->nv.size;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  PGX_CU(p_cuMulticastCreate(&x->nv.mc, &mp));
+  int fd = -1;
+  PGX_CU(p_cuMemExportToShareableHandle(&fd, x->nv.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  *fd_out = fd;
+  return PGX_OK;
+}
+
+extern "C" int pgx_xchg_nvls_import(pgx_xchg* x, int fd) {
+  PGX_DRV(cuMemImportFromShareableHandle);
+  PGX_DRV(cuMulticastAddDevice);
+  PGX_DRV(cuDeviceGet);
+  if (!p_cuMemImportFromShareableHandle || !p_cuMulticastAddDevice || !p_cuDeviceGet)
+    return fail(PGX_E_CUDA, "multicast entry points");
+  if (x->rank != 0) {
+    if (fd < 0) return fail(PGX_E_CONFIG, "no multicast handle received");
+    PGX_CU(p_cuMemImportFromShareableHandle(&x->nv.mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+    close(fd);
+  }
+  CUdevice d;
+  PGX_CU(p_cuDeviceGet(&d, x->dev));
+  PGX_CU(p_cuMulticastAddDevice(x->nv.mc, d));
+  return PGX_OK;
+}
+
+// After EVERY rank added its device: bind local memory, map unicast + multicast views,
+// move the weights into the multicast-backed buffer (the model the framework aliases).
+extern "C" int pgx_xchg_nvls_bind(pgx_xchg* x) {
+  PGX_DRV(cuMemCreate);
+  PGX_DRV(cuMulticastBindMem);
+  PGX_DRV(cuMemAddressReserve);
+  PGX_DRV(cuMemMap);
+  PGX_DRV(cuMemSetAccess);
+  if (!p_cuMemCreate || !p_cuMulticastBindMem || !p_cuMemAddressReserve || !p_cuMemMap || !p_cuMemSetAccess)
+    return fail(PGX_E_CUDA, "multicast entry points");
+  int prev;
+  cudaGetDevice(&prev);
+  cudaSetDevice(x->dev);
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = x->dev;
+  PGX_CU(p_cuMemCreate(&x->nv.mem, x->nv.size, &ap, 0));
+  PGX_CU(p_cuMulticastBindMem(x->nv.mc, 0, x->nv.mem, 0, x->nv.size, 0));
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = x->dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  PGX_CU(p_cuMemAddressReserve(&x->nv.uc, x->nv.size, 0, 0, 0));
+  PGX_CU(p_cuMemMap(x->nv.uc, x->nv.size, 0, x->nv.mem, 0));
+  PGX_CU(p_cuMemSetAccess(x->nv.uc, x->nv.size, &acc, 1));
+  PGX_CU(p_cuMemAddressReserve(&x->nv.mcp, x->nv.size, 0, 0, 0));
+  PGX_CU(p_cuMemMap(x->nv.mcp, x->nv.size, 0, x->nv.mc, 0));
+  PGX_CU(p_cuMemSetAccess(x->nv.mcp, x->nv.size, &acc, 1));
+  PGX_CUDA(cudaMemset((void*)x->nv.uc, 0, x->nv.size));
+  uint64_t model_bytes = x->nv.grad_off;
+  PGX_CUDA(cudaMemcpy((void*)x->nv.uc, x->model, model_bytes, cudaMemcpyDeviceToDevice));
+  PGX_CUDA(cudaMalloc(&x->nv.pub_count, x->L.size() * sizeof(uint32_t)));
+  PGX_CUDA(cudaMemset(x->nv.pub_count, 0, x->L.size() * sizeof(uint32_t)));
+  x->model = (void*)x->nv.uc;
+  x->nv.on = true;
+  // gate table: arrival counters live in the multicast-backed flags now
+  std::vector<GateEntry> ents;
+  for (size_t l = 0; l < x->L.size(); ++l)
+    ents.push_back({reinterpret_cast<uint32_t*>(x->nv.uc + x->nv.flag_off + l * 256 + 128), x->L[l].expected});
+  PGX_CUDA(cudaMemcpy(x->gate_table, ents.data(), ents.size() * sizeof(GateEntry), cudaMemcpyHostToDevice));
+  x->gate_entries = (int)ents.size();
+  PGX_CUDA(cudaDeviceSynchronize());
+  cudaSetDevice(prev);
+  return PGX_OK;
+}
+
+static void nvls_release(pgx_xchg* x) {
+  if (!x->nv.mc) return;
+  PGX_DRV(cuMemUnmap);
+  PGX_DRV(cuMemAddressFree);
+  PGX_DRV(cuMemRelease);
+  PGX_DRV(cuMulticastUnbind);
+  PGX_DRV(cuDeviceGet);
+  if (x->nv.mcp && p_cuMemUnmap) p_cuMemUnmap(x->nv.mcp, x->nv.size);
+  if (x->nv.uc && p_cuMemUnmap) p_cuMemUnmap(x->nv.uc, x->nv.size);
+  if (x->nv.mcp && p_cuMemAddressFree) p_cuMemAddressFree(x->nv.mcp, x->nv.size);
+  if (x->nv.uc && p_cuMemAddressFree) p_cuMemAddressFree(x->nv.uc, x->nv.size);
+  CUdevice d;
+  if (x->nv.mem && p_cuMulticastUnbind && p_cuDeviceGet && p_cuDeviceGet(&d, x->dev) == CUDA_SUCCESS)
+    p_cuMulticastUnbind(x->nv.mc, d, 0, x->nv.size);
+  if (x->nv.mem && p_cuMemRelease) p_cuMemRelease(x->nv.mem);
+  if (p_cuMemRelease) p_cuMemRelease(x->nv.mc);
+  if (x->nv.pub_count) cudaFree(x->nv.pub_count);
+  x->nv = pgx_xchg::Nvls{};
+}
+
+static int launch_nvls(pgx_xchg* x, int l, const LayerPlan& P, const XArgs& a, cudaStream_t s) {
+  if (!x->nv.on) return fail(PGX_E_CONFIG, "NVLS exchange not bound (pgx_xchg_nvls_bind)");
+  NvArgs n;
+  memset(&n, 0, sizeof(n));
+  n.g = a.g;
+  n.uc_model = reinterpret_cast<float*>(x->nv.uc) + P.model_off;
+  n.uc_grad = reinterpret_cast<float*>(x->nv.uc + x->nv.grad_off) + P.model_off;
+  n.mc_model = x->nv.mcp + P.model_off * 4;
+  n.mc_grad = x->nv.mcp + x->nv.grad_off + P.model_off * 4;
+  n.uc_ready = reinterpret_cast<uint32_t*>(x->nv.uc + x->nv.flag_off + (uint64_t)l * 256);
+  n.mc_ready = x->nv.mcp + x->nv.flag_off + (uint64_t)l * 256;
+  n.mc_arrive = n.mc_ready + 128;
+  n.pub_count = x->nv.pub_count + l;
+  n.v = a.v;
+  n.queue = a.queue;
+  n.S = P.S;
+  n.sl = P.sl;
+  n.CH = x->cfg.chunk_elems;
+  n.pub_items = P.push_items;
+  n.items = P.items;
+  n.epoch = a.epoch;
+  n.iter = a.iter;
+  n.rank = x->rank;
+  n.world = x->world;
+  n.lr = a.lr;
+  n.scale = a.scale;
+  n.mu = a.mu;
+  n.wd = a.wd;
+  n.st = a.st;
+  ++x->launches;
+  k_nvls<<<P.grid, kThreads, 0, s>>>(n);
+  return PGX_OK;
+}
 
 // TWOSHOT_CE launch: reduce-scatter and all-gather as peer DMA copies, each batch
 // followed (in stream order) by k_signal raising the peers' notifications with a
@@ -931,7 +1259,11 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     P.variant = cfg->variant ? cfg->variant[l] : PGX_VARIANT_TWOSHOT;
     P.model_off = moff;
     moff = align_up(moff + P.S, kAlignElems);
-    if (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CE) {
+    if (P.variant == PGX_VARIANT_NVLS && (cfg->mode != PGX_MODE_FAST32 || N < 2)) {
+      delete x;
+      return fail(PGX_E_CONFIG, "NVLS layers need fast32 and at least 2 ranks");
+    }
+    if (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CE || P.variant == PGX_VARIANT_NVLS) {
       P.sl = align_up((P.S + N - 1) / N, 4);
       P.C = (uint32_t)((P.sl + CH - 1) / CH);
       P.K = N;
@@ -950,13 +1282,19 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
         remote += (uint32_t)((hi - lo + CH - 1) / CH);
       }
       P.expected = remote;
+      if (P.variant == PGX_VARIANT_NVLS) {  // publish every chunk of the layer, then own chunks
+        uint32_t Cf = (uint32_t)((P.S + CH - 1) / CH);
+        P.push_items = Cf;
+        P.items = Cf + P.C;
+        P.expected = remote + my_chunks;  // every owner's chunks arrive by multicast, own ones included
+      }
       P.grid = (int)std::min<uint64_t>(P.items, cfg->max_ctas > 0 ? cap : (N == 1 ? 4 * sms : cap));
       uint64_t own = my_hi - my_lo;
       P.nvlink_bytes = (N > 1) ? 2ull * (P.S - own) * x->esz : 0;  // RS out + AG out
       // owner fold: N partial reads + w (+v) read/write; pushes read the rest of the gradient
       P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0)) * own * x->esz +
                     (P.S - own) * x->esz;
-      (void)my_chunks;
+
     } else if (P.variant == PGX_VARIANT_TREE) {
       P.sl = align_up(P.S, kAlignElems);  // slot stride keeps every slot 16B-aligned
       P.C = (uint32_t)((P.S + CH - 1) / CH);
@@ -1078,6 +1416,7 @@ int pgx_xchg_destroy(pgx_xchg* x) {
     for (auto& e : v) cudaEventDestroy(e.e);
   if (x->iter_dev) cudaFree(x->iter_dev);
   if (x->gate_table) cudaFree(x->gate_table);
+  nvls_release(x);
   if (x->own_streams) {
     if (x->down) cudaStreamDestroy(x->down);
     if (x->ce_rs) cudaStreamDestroy(x->ce_rs);
@@ -1131,6 +1470,13 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
   int prev;
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
+  if (P.variant == PGX_VARIANT_NVLS) {
+    xrecord(x->ready[l], s);
+    int rc = launch_nvls(x, l, P, a, s);
+    if (rc == PGX_OK) xrecord(x->done[l], s);
+    if (prev != x->dev) cudaSetDevice(prev);
+    return rc;
+  }
   if (P.variant == PGX_VARIANT_TWOSHOT_CE) {
     int rc = launch_twoshot_ce(x, l, P, a, s, phases);
     if (prev != x->dev) cudaSetDevice(prev);
@@ -1208,7 +1554,10 @@ int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
     }
   } else if (e == cudaSuccess && P.expected) {
     ++x->launches;
-    k_gate<<<1, 32, 0, s>>>(x->mflags + l, (iteration + 1) * P.expected, it, iteration + 1, P.expected,
+    const uint32_t* counter = x->mflags + l;
+    if (P.variant == PGX_VARIANT_NVLS)
+      counter = reinterpret_cast<const uint32_t*>(x->nv.uc + x->nv.flag_off + (uint64_t)l * 256 + 128);
+    k_gate<<<1, 32, 0, s>>>(counter, (iteration + 1) * P.expected, it, iteration + 1, P.expected,
                             world_status(x->w));
     e = cudaGetLastError();
   }

@@ -23,7 +23,8 @@ import torch
 from . import _lib
 from .errors import ConfigError, ShapeError
 
-VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE}
+VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
+            "nvls": _lib.VARIANT_NVLS}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32}
 
 
@@ -83,6 +84,12 @@ class DeviceExchange:
         seg = transport.segment(seg_base)
         eb = torch.empty((), dtype=self.dtype).element_size()
         self.model = seg.data[: (seg.size // eb) * eb].view(self.dtype)
+        if "nvls" in variants:
+            self._nvls_setup()  # the weights move into the multicast-backed buffer
+            _lib.call("pgx_xchg_model", h, C.byref(mp), offs)
+            from .transport import _CudaArray
+            self._nvls_model = torch.as_tensor(_CudaArray(mp.value, seg.size, self), device=transport.device)
+            self.model = self._nvls_model[: (seg.size // eb) * eb].view(self.dtype)
         self.layer_views = [self.model[o:o + n] for o, n in zip(self.model_offsets, self.layer_elems)]
         with torch.cuda.device(transport.device):
             self.stream = torch.cuda.Stream(device=transport.device, priority=-1)
@@ -96,6 +103,45 @@ class DeviceExchange:
                                      for _ in range(_lib.XCHG_STREAMS)]
         arr = (C.c_void_p * _lib.XCHG_STREAMS)(*[s.cuda_stream for s in self.internal_streams])
         _lib.call("pgx_xchg_set_streams", h, arr, _lib.XCHG_STREAMS)
+
+    def _nvls_setup(self) -> None:
+        """Collective: rank 0's multicast handle reaches every rank as a file descriptor over
+        a Unix socket (SCM_RIGHTS); every rank adds its GPU; after all did, bind memory."""
+        import os
+        import socket
+
+        import torch.distributed as dist
+
+        if self.world < 2 or not dist.is_initialized():
+            raise ConfigError("the NVLS variant needs >= 2 ranks in an initialised torch.distributed group")
+        fd = C.c_int(-1)
+        _lib.call("pgx_xchg_nvls_export", self.handle, C.byref(fd))
+        token = [f"pgx-nvls-{os.getpid()}-{id(self)}" if self.rank == 0 else None]
+        dist.broadcast_object_list(token, src=0)
+        addr = "\0" + token[0]
+        if self.rank == 0:
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(addr)
+            srv.listen(self.world)
+            dist.barrier()
+            for _ in range(self.world - 1):
+                conn, _ = srv.accept()
+                socket.send_fds(conn, [b"x"], [fd.value])
+                conn.close()
+            srv.close()
+            os.close(fd.value)
+            got = -1
+        else:
+            dist.barrier()
+            cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            cli.connect(addr)
+            _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+            cli.close()
+            got = fds[0]
+        _lib.call("pgx_xchg_nvls_import", self.handle, got)
+        dist.barrier()  # every GPU joined the multicast team before anyone binds
+        _lib.call("pgx_xchg_nvls_bind", self.handle)
+        dist.barrier()
 
     # -- wiring ----------------------------------------------------------------
     def connect(self) -> None:
