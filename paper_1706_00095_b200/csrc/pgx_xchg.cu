@@ -983,6 +983,7 @@ static int nvls_granularity(pgx_xchg* x, size_t* gran) {
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = x->dev;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   PGX_CU(p_cuMemGetAllocationGranularity(&g2, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
   *gran = std::max(g1, g2);
   return PGX_OK;
@@ -1045,8 +1046,13 @@ extern "C" int pgx_xchg_nvls_bind(pgx_xchg* x) {
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = x->dev;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // multicast binding needs a shareable type
   PGX_CU(p_cuMemCreate(&x->nv.mem, x->nv.size, &ap, 0));
-  PGX_CU(p_cuMulticastBindMem(x->nv.mc, 0, x->nv.mem, 0, x->nv.size, 0));
+  {
+    CUresult r = p_cuMulticastBindMem(x->nv.mc, 0, x->nv.mem, 0, x->nv.size, 0);
+    if (r != CUDA_SUCCESS)
+      return fail(PGX_E_CUDA, "cuMulticastBindMem failed (CUresult %d, size %zu)", (int)r, x->nv.size);
+  }
   CUmemAccessDesc acc{};
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   acc.location.id = x->dev;
