@@ -335,7 +335,7 @@ __device__ __forceinline__ uint64_t tma_copy(uint8_t* dst, const uint8_t* src, u
 // kTma (N > 1): push chunks and all-gather tiles move as TMA bulk copies through a
 // 64 KB shared-memory buffer (dynamic smem), driven by thread 0.
 template <int N, class T, bool kTma>
-__global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
+__global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot(XArgs a) {
   constexpr int W = VecT<T>::W;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kThreads) k_twoshot(XArgs a) {
       cta_wait_flags(s_flags, N - 1, epoch, a.st);
       const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
       uint64_t nvec = (hi - lo + W - 1) / W;
-      constexpr int U = N <= 4 ? 2 : 1;
+      constexpr int U = N <= 2 ? 2 : 1;  // 2 CTAs/SM (64 regs) without spills
       if constexpr (kTma) {
         T* tile = reinterpret_cast<T*>(tma_buf);
         for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
