@@ -575,12 +575,12 @@ struct NvArgs {
   float* uc_model;            // layer base, local mapping
   float* uc_grad;             // layer base, local mapping
   uint64_t mc_model, mc_grad; // layer base, multicast mapping
-  uint32_t* uc_ready;         // this layer's "all ranks published" counter (local view)
+  uint32_t* uc_ready;         // this layer's ready[owner][chunk] counters (local view)
   uint64_t mc_ready, mc_arrive;
-  uint32_t* pub_count;        // local: publish chunks completed (monotonic)
   float* v;
   uint32_t* queue;
   uint64_t S, sl, CH;
+  uint32_t C;                 // chunks per shard
   uint32_t pub_items, items, epoch;
   const uint32_t* iter;
   int rank, world;
@@ -621,31 +621,41 @@ __device__ __forceinline__ float fast32_update(float w, float g, float& v, const
   return __fsub_rn(w, vv);
 }
 
-__global__ void __launch_bounds__(kThreads) k_nvls(NvArgs a) {
+// Items: publish (chunk c of owner j's shard, c-major so early chunks of every shard go
+// first) -> ready[j][c] += 1 on every GPU (multimem.red); owner chunk c of my shard waits
+// ready[me][c] >= N*epoch, so publish and reduction pipeline chunk by chunk.
+__global__ void __launch_bounds__(kThreads, 1) k_nvls(NvArgs a) {
   __shared__ uint32_t s_item;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
-  const int me = a.rank;
-  const uint32_t pub_chunks = a.pub_items;
+  const int me = a.rank, N = a.world;
   while (true) {
     uint32_t it = claim(a.queue, &s_item);
     if (it >= a.items) break;
     if (it < a.pub_items) {
-      // ---- publish: this chunk of my gradient into my slice of the multicast object
-      uint64_t lo = (uint64_t)it * a.CH, hi = min(lo + a.CH, a.S);
-      for (uint64_t e = lo + threadIdx.x * 4; e < hi; e += (uint64_t)blockDim.x * 4) {
-        int cnt = (int)min((uint64_t)4, hi - e);
-        float buf[4];
-        grad_vec<float>(a.g, e, cnt, buf);
-        st_vec<float>(a.uc_grad + e, cnt, buf);
+      // ---- publish chunk c of owner j's shard into my slice of the multicast object
+      uint32_t c = it / (uint32_t)N;
+      int j = it % N;
+      uint64_t lo = j * a.sl + (uint64_t)c * a.CH;
+      uint64_t hi = min(min(lo + a.CH, (uint64_t)(j + 1) * a.sl), a.S);
+      if (lo >= hi) continue;
+      constexpr int UP = 4;
+      for (uint64_t e0 = lo + threadIdx.x * 4; e0 < hi; e0 += (uint64_t)UP * blockDim.x * 4) {
+        float buf[UP][4];
+        int cnt[UP];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+          uint64_t e = e0 + (uint64_t)u * blockDim.x * 4;
+          cnt[u] = e < hi ? (int)min((uint64_t)4, hi - e) : 0;
+          if (cnt[u] > 0) grad_vec<float>(a.g, e, cnt[u], buf[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < UP; ++u)
+          if (cnt[u] > 0) st_vec<float>(a.uc_grad + e0 + (uint64_t)u * blockDim.x * 4, cnt[u], buf[u]);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
         fence_acq_rel_sys();
-        uint32_t done = atomicAdd(a.pub_count, 1u) + 1;
-        if (done == pub_chunks) {  // my whole layer is published (the next launch is stream-ordered)
-          *a.pub_count = 0;
-          mm_red_release_add(a.mc_ready, 1u);
-        }
+        mm_red_release_add(a.mc_ready + ((uint64_t)j * a.C + c) * 4, 1u);
       }
     } else {
       // ---- owner chunk: switch-reduced gradient, fused update, multicast store of the weights
@@ -653,28 +663,45 @@ __global__ void __launch_bounds__(kThreads) k_nvls(NvArgs a) {
       uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
       uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
       if (lo >= hi) continue;
-      if (threadIdx.x == 0) wait_geq(a.uc_ready, epoch * (uint32_t)a.world, a.st);
+      if (threadIdx.x == 0) wait_geq(a.uc_ready + (uint64_t)me * a.C + c, epoch * (uint32_t)N, a.st);
       __syncthreads();
-      for (uint64_t e = lo + threadIdx.x * 4; e < hi; e += (uint64_t)blockDim.x * 4) {
-        if (e + 4 <= hi) {
-          float4 g = mm_ld_reduce4(a.mc_grad + e * 4);
-          float4 w = __ldcg(reinterpret_cast<const float4*>(a.uc_model + e));
-          float4 v = *reinterpret_cast<const float4*>(a.v + e);
-          w.x = fast32_update(w.x, g.x, v.x, a);
-          w.y = fast32_update(w.y, g.y, v.y, a);
-          w.z = fast32_update(w.z, g.z, v.z, a);
-          w.w = fast32_update(w.w, g.w, v.w, a);
-          *reinterpret_cast<float4*>(a.v + e) = v;
-          mm_st4(a.mc_model + e * 4, w);
-        } else {
-          for (uint64_t k = e; k < hi; ++k) {
-            float g = mm_ld_reduce1(a.mc_grad + k * 4);
-            float w = __ldcg(a.uc_model + k), v = a.v[k];
-            w = fast32_update(w, g, v, a);
-            a.v[k] = v;
-            mm_st1(a.mc_model + k * 4, w);
+      constexpr int U = 4;
+      uint64_t body = lo + (hi - lo) / 4 * 4;
+      for (uint64_t e0 = lo + threadIdx.x * 4; e0 < body; e0 += (uint64_t)U * blockDim.x * 4) {
+        float4 g[U], w[U], v[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint64_t e = e0 + (uint64_t)u * blockDim.x * 4;
+          ok[u] = e < body;
+          if (ok[u]) g[u] = mm_ld_reduce4(a.mc_grad + e * 4);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          uint64_t e = e0 + (uint64_t)u * blockDim.x * 4;
+          if (ok[u]) {
+            w[u] = __ldcg(reinterpret_cast<const float4*>(a.uc_model + e));
+            v[u] = *reinterpret_cast<const float4*>(a.v + e);
           }
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) continue;
+          uint64_t e = e0 + (uint64_t)u * blockDim.x * 4;
+          w[u].x = fast32_update(w[u].x, g[u].x, v[u].x, a);
+          w[u].y = fast32_update(w[u].y, g[u].y, v[u].y, a);
+          w[u].z = fast32_update(w[u].z, g[u].z, v[u].z, a);
+          w[u].w = fast32_update(w[u].w, g[u].w, v[u].w, a);
+          *reinterpret_cast<float4*>(a.v + e) = v[u];
+          mm_st4(a.mc_model + e * 4, w[u]);
+        }
+      }
+      for (uint64_t k = body + threadIdx.x; k < hi; k += blockDim.x) {  // ragged end of the layer
+        float g = mm_ld_reduce1(a.mc_grad + k * 4);
+        float w = __ldcg(a.uc_model + k), v = a.v[k];
+        w = fast32_update(w, g, v, a);
+        a.v[k] = v;
+        mm_st1(a.mc_model + k * 4, w);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -840,7 +867,7 @@ struct pgx_xchg {
     CUmemGenericAllocationHandle mc = 0, mem = 0;
     CUdeviceptr uc = 0, mcp = 0;                   // unicast (local) and multicast mappings
     uint64_t grad_off = 0, flag_off = 0;           // bytes
-    uint32_t* pub_count = nullptr;                 // local per-layer publish-completion counters
+    std::vector<uint64_t> fl;                      // per layer: [arrive | ready[N][C]] offset in the flags
   } nv;
 };
 
@@ -964,7 +991,13 @@ static size_t nvls_size(pgx_xchg* x, size_t gran) {
   model_bytes = (model_bytes + 255) / 256 * 256;
   x->nv.grad_off = model_bytes;
   x->nv.flag_off = 2 * model_bytes;
-  size_t total = 2 * model_bytes + x->L.size() * 256;
+  x->nv.fl.clear();
+  uint64_t f = 0;
+  for (auto& P : x->L) {  // [arrive counter (128 B) | ready[N][C] u32]
+    x->nv.fl.push_back(f);
+    f += 128 + ((uint64_t)x->world * P.C * 4 + 127) / 128 * 128;
+  }
+  size_t total = 2 * model_bytes + f;
   return (total + gran - 1) / gran * gran;
 }
 
@@ -1066,14 +1099,12 @@ extern "C" int pgx_xchg_nvls_bind(pgx_xchg* x) {
   PGX_CUDA(cudaMemset((void*)x->nv.uc, 0, x->nv.size));
   uint64_t model_bytes = x->nv.grad_off;
   PGX_CUDA(cudaMemcpy((void*)x->nv.uc, x->model, model_bytes, cudaMemcpyDeviceToDevice));
-  PGX_CUDA(cudaMalloc(&x->nv.pub_count, x->L.size() * sizeof(uint32_t)));
-  PGX_CUDA(cudaMemset(x->nv.pub_count, 0, x->L.size() * sizeof(uint32_t)));
   x->model = (void*)x->nv.uc;
   x->nv.on = true;
   // gate table: arrival counters live in the multicast-backed flags now
   std::vector<GateEntry> ents;
   for (size_t l = 0; l < x->L.size(); ++l)
-    ents.push_back({reinterpret_cast<uint32_t*>(x->nv.uc + x->nv.flag_off + l * 256 + 128), x->L[l].expected});
+    ents.push_back({reinterpret_cast<uint32_t*>(x->nv.uc + x->nv.flag_off + x->nv.fl[l]), x->L[l].expected});
   PGX_CUDA(cudaMemcpy(x->gate_table, ents.data(), ents.size() * sizeof(GateEntry), cudaMemcpyHostToDevice));
   x->gate_entries = (int)ents.size();
   PGX_CUDA(cudaDeviceSynchronize());
@@ -1097,7 +1128,6 @@ static void nvls_release(pgx_xchg* x) {
     p_cuMulticastUnbind(x->nv.mc, d, 0, x->nv.size);
   if (x->nv.mem && p_cuMemRelease) p_cuMemRelease(x->nv.mem);
   if (p_cuMemRelease) p_cuMemRelease(x->nv.mc);
-  if (x->nv.pub_count) cudaFree(x->nv.pub_count);
   x->nv = pgx_xchg::Nvls{};
 }
 
@@ -1110,10 +1140,10 @@ static int launch_nvls(pgx_xchg* x, int l, const LayerPlan& P, const XArgs& a, c
   n.uc_grad = reinterpret_cast<float*>(x->nv.uc + x->nv.grad_off) + P.model_off;
   n.mc_model = x->nv.mcp + P.model_off * 4;
   n.mc_grad = x->nv.mcp + x->nv.grad_off + P.model_off * 4;
-  n.uc_ready = reinterpret_cast<uint32_t*>(x->nv.uc + x->nv.flag_off + (uint64_t)l * 256);
-  n.mc_ready = x->nv.mcp + x->nv.flag_off + (uint64_t)l * 256;
-  n.mc_arrive = n.mc_ready + 128;
-  n.pub_count = x->nv.pub_count + l;
+  n.uc_ready = reinterpret_cast<uint32_t*>(x->nv.uc + x->nv.flag_off + x->nv.fl[l] + 128);
+  n.mc_ready = x->nv.mcp + x->nv.flag_off + x->nv.fl[l] + 128;
+  n.mc_arrive = x->nv.mcp + x->nv.flag_off + x->nv.fl[l];
+  n.C = P.C;
   n.v = a.v;
   n.queue = a.queue;
   n.S = P.S;
@@ -1288,10 +1318,9 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
         remote += (uint32_t)((hi - lo + CH - 1) / CH);
       }
       P.expected = remote;
-      if (P.variant == PGX_VARIANT_NVLS) {  // publish every chunk of the layer, then own chunks
-        uint32_t Cf = (uint32_t)((P.S + CH - 1) / CH);
-        P.push_items = Cf;
-        P.items = Cf + P.C;
+      if (P.variant == PGX_VARIANT_NVLS) {  // publish (owner, chunk) items, then own chunks
+        P.push_items = (uint32_t)N * P.C;
+        P.items = P.push_items + P.C;
         P.expected = remote + my_chunks;  // every owner's chunks arrive by multicast, own ones included
       }
       P.grid = (int)std::min<uint64_t>(P.items, cfg->max_ctas > 0 ? cap : (N == 1 ? 4 * sms : cap));
@@ -1562,7 +1591,7 @@ int pgx_xchg_gate(pgx_xchg* x, int l, uint32_t iteration, void* stream) {
     ++x->launches;
     const uint32_t* counter = x->mflags + l;
     if (P.variant == PGX_VARIANT_NVLS)
-      counter = reinterpret_cast<const uint32_t*>(x->nv.uc + x->nv.flag_off + (uint64_t)l * 256 + 128);
+      counter = reinterpret_cast<const uint32_t*>(x->nv.uc + x->nv.flag_off + x->nv.fl[l]);
     k_gate<<<1, 32, 0, s>>>(counter, (iteration + 1) * P.expected, it, iteration + 1, P.expected,
                             world_status(x->w));
     e = cudaGetLastError();
