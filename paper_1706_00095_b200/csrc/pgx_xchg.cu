@@ -624,6 +624,9 @@ __device__ __forceinline__ float fast32_update(float w, float g, float& v, const
 // Items: publish (chunk c of owner j's shard, c-major so early chunks of every shard go
 // first) -> ready[j][c] += 1 on every GPU (multimem.red); owner chunk c of my shard waits
 // ready[me][c] >= N*epoch, so publish and reduction pipeline chunk by chunk.
+#ifndef NVLS_U
+#define NVLS_U 8  // multimem.ld_reduce in flight per thread
+#endif
 __global__ void __launch_bounds__(kThreads, 1) k_nvls(NvArgs a) {
   __shared__ uint32_t s_item;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
@@ -665,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_nvls(NvArgs a) {
       if (lo >= hi) continue;
       if (threadIdx.x == 0) wait_geq(a.uc_ready + (uint64_t)me * a.C + c, epoch * (uint32_t)N, a.st);
       __syncthreads();
-      constexpr int U = 4;
+      constexpr int U = NVLS_U;
       uint64_t body = lo + (hi - lo) / 4 * 4;
       for (uint64_t e0 = lo + threadIdx.x * 4; e0 < body; e0 += (uint64_t)U * blockDim.x * 4) {
         float4 g[U], w[U], v[U];
