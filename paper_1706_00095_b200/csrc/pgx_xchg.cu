@@ -625,9 +625,12 @@ __device__ __forceinline__ float fast32_update(float w, float g, float& v, const
 // first) -> ready[j][c] += 1 on every GPU (multimem.red); owner chunk c of my shard waits
 // ready[me][c] >= N*epoch, so publish and reduction pipeline chunk by chunk.
 #ifndef NVLS_U
-#define NVLS_U 8  // multimem.ld_reduce in flight per thread
+#define NVLS_U 2  // multimem.ld_reduce in flight per thread (r1v: 4 -> 882 us, r1w: 8 -> 965 us @ 256 MB, N=4)
 #endif
-__global__ void __launch_bounds__(kThreads, 1) k_nvls(NvArgs a) {
+#ifndef NVLS_MINB
+#define NVLS_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, NVLS_MINB) k_nvls(NvArgs a) {
   __shared__ uint32_t s_item;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int me = a.rank, N = a.world;
