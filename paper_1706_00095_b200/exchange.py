@@ -198,6 +198,16 @@ class DeviceExchange:
         """Make `stream` wait until this rank's part of layer's last exchange is done."""
         _lib.call("pgx_xchg_join", self.handle, layer, stream.cuda_stream)
 
+    def check(self) -> None:
+        """Raise TransportError if a bounded device wait expired (a peer died or the
+        protocol wedged) — the device-side analog of finalize's watchdog (pipelined.py:60-80)."""
+        status = self.tr.device_status()
+        if status:
+            from .errors import TransportError
+
+            raise TransportError(f"rank {self.rank}: device wait expired (status {status}); a peer stopped "
+                                 "contributing or the exchange protocol wedged")
+
     def launch_count(self) -> int:
         """Kernels launched by this exchange so far (exchange + gate kernels)."""
         n = C.c_uint64()
@@ -324,8 +334,9 @@ class ModuleBinding:
         return pre_hook
 
     def step_done(self) -> None:
-        """Call once per iteration after backward()."""
+        """Call once per iteration after backward(); raises if a device wait expired."""
         self.k += 1
+        self.x.check()
 
     def begin_step(self) -> None:
         """Graph mode: advance the device iteration counter (capture this first)."""

@@ -262,3 +262,50 @@ def test_real_models_match_oracle(which, variant, gate):
     out = _spawn(_model_worker, world, which, variant, gate)
     for rank, bad, status in out:
         assert bad == [] and status == 0, (rank, bad, status)
+
+
+def _fault_worker(rank, world, port, variant, q):
+    """Rank 1 stops contributing after iteration 0; rank 0's bounded device waits must expire
+    and surface as TransportError instead of hanging (fault injection, test_transport_tcp.py:134-160)."""
+    import time
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    from paper_1706_00095_b200.errors import TransportError
+    from paper_1706_00095_b200.exchange import DeviceExchange
+    from paper_1706_00095_b200.transport import DistTransport
+
+    outcome = "no error"
+    try:
+        tr = DistTransport(rank, world, rank, timeout_s=2.0)
+        x = DeviceExchange(tr, [1 << 16], mode="fast32", variant=variant, lr=0.01)
+        tr.barrier()
+        x.connect()
+        g = torch.ones(1 << 16, device="cuda")
+        for k in range(2):
+            if k == 1 and rank == 1:
+                break  # the "dead" peer
+            x.launch(0, k, [g])
+            x.gate(0, k)
+            torch.cuda.synchronize()
+        t0 = time.time()
+        try:
+            x.check()
+        except TransportError as exc:
+            outcome = f"TransportError after {time.time() - t0:.1f}s: {exc}"
+    except Exception as exc:  # noqa: BLE001
+        outcome = repr(exc)
+    q.put((rank, outcome, 0))
+    dist.barrier()  # keep the peer's memory mapped until everyone is done
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce"])
+def test_dead_peer_surfaces_as_transport_error(variant):
+    out = _spawn(_fault_worker, 2, variant)
+    assert out[0][1].startswith("TransportError"), out
+    assert out[1][1] == "no error", out
