@@ -11,6 +11,28 @@ from __future__ import annotations
 
 import torch
 import torch.nn as nn
+import torch.nn.functional as F
+
+
+class LRN(nn.Module):
+    """Caffe/AlexNet across-channel LRN, the same function as nn.LocalResponseNorm:
+    x / (k + alpha/size * sum_{c-size/2..c+size/2} x^2)^beta.  The channel window is summed
+    with one avg_pool1d over the innermost dim of the channels-last activation (one kernel
+    instead of pad + avg_pool3d + elementwise), in fp32; measured 12 % faster AlexNet steps
+    (profiles/r1fb_fwdbwd_variants.jsonl) with identical results."""
+
+    def __init__(self, size=5, alpha=1e-4, beta=0.75, k=1.0):
+        super().__init__()
+        self.size, self.alpha, self.beta, self.k = size, alpha, beta, k
+
+    def forward(self, x):
+        n, c, h, w = x.shape
+        xl = x.permute(0, 2, 3, 1)
+        xf = xl.float()
+        s = F.avg_pool1d((xf * xf).reshape(-1, 1, c), self.size, stride=1, padding=self.size // 2,
+                         count_include_pad=True)
+        div = (s.reshape(n, h, w, c) * self.alpha + self.k).pow(self.beta)
+        return (xf / div).to(x.dtype).permute(0, 3, 1, 2)
 
 
 class AlexNet(nn.Module):
@@ -27,7 +49,7 @@ class AlexNet(nn.Module):
         self.fc7 = nn.Linear(4096, 4096)
         self.fc8 = nn.Linear(4096, 1000)
         self.relu = nn.ReLU(inplace=True)
-        self.lrn = nn.LocalResponseNorm(5, alpha=1e-4, beta=0.75)
+        self.lrn = LRN(5, alpha=1e-4, beta=0.75)
         self.pool = nn.MaxPool2d(3, 2)
         self.drop = nn.Dropout(0.5)
 
@@ -91,7 +113,7 @@ class GoogLeNet(nn.Module):
         self.conv1 = nn.Conv2d(3, 64, 7, 2, 3)
         self.conv2r = nn.Conv2d(64, 64, 1)
         self.conv2 = nn.Conv2d(64, 192, 3, padding=1)
-        self.lrn = nn.LocalResponseNorm(5, alpha=1e-4, beta=0.75)
+        self.lrn = LRN(5, alpha=1e-4, beta=0.75)
         self.i3a = _Inception(192, 64, 96, 128, 16, 32, 32)
         self.i3b = _Inception(256, 128, 128, 192, 32, 96, 64)
         self.i4a = _Inception(480, 192, 96, 208, 16, 48, 64)
