@@ -49,7 +49,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "nvls", "auto", "nccl_bulk", "ddp"],
+    p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "nvls", "oneshot", "auto", "nccl_bulk", "ddp"],
                    help="nccl_bulk / ddp are comparison rows (NCCL on the path), not the product")
     p.add_argument("--chunk-elems", type=int, default=16384)
     p.add_argument("--gate", default="auto", choices=["auto", "layer", "model"],
@@ -425,7 +425,8 @@ def pgx_arm(args):
     nvl, hbm = xchg.layer_bytes(L_DOM)
     avg = statistics.mean(durs) if durs else None
     kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local + copy-engine transfers",
-             "tree": "k_tree_up/k_tree_down", "nvls": "k_nvls (multimem)"}[xchg.variants[L_DOM]]
+             "tree": "k_tree_up/k_tree_down", "nvls": "k_nvls (multimem)",
+             "oneshot": "k_oneshot"}[xchg.variants[L_DOM]]
     what = "%s, layer %d (%d params): fold + fused momentum update%s" % (
         kname, L_DOM, sizes[L_DOM], " + reduce-scatter/all-gather over NVLink" if world > 1 else "")
     measured_in = (("CUDA events captured in the step graph, %d replays after the timed region" % len(durs))

@@ -164,8 +164,10 @@ enum pgx_variant {
   PGX_VARIANT_TREE = 0,       /* paper: binomial reduce + master update + broadcast     */
   PGX_VARIANT_TWOSHOT = 1,    /* SM peer stores: reduce-scatter, owner update, gather   */
   PGX_VARIANT_TWOSHOT_CE = 2, /* same schedule, shards moved by the copy engines        */
-  PGX_VARIANT_NVLS = 3        /* NVLink SHARP: in-switch reduce (multimem.ld_reduce) +
+  PGX_VARIANT_NVLS = 3,       /* NVLink SHARP: in-switch reduce (multimem.ld_reduce) +
                                  multicast weight store; fast32 only, tolerance parity  */
+  PGX_VARIANT_ONESHOT = 4     /* small layers: everyone pushes everything once, every
+                                 rank folds (same order) and updates its own copy       */
 };
 
 typedef struct pgx_xchg_config {

@@ -24,7 +24,7 @@ MAX_PIECES = 4
 XCHG_STREAMS = 5
 
 MODE_REF64, MODE_REF32, MODE_FAST32 = 0, 1, 2
-VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE, VARIANT_NVLS = 0, 1, 2, 3
+VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE, VARIANT_NVLS, VARIANT_ONESHOT = 0, 1, 2, 3, 4
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p

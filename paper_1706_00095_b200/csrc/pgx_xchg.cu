@@ -458,6 +458,56 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
   retire(a.queue);
 }
 
+// ============================================================== ONESHOT
+// Small layers are latency-bound: every rank pushes its whole gradient to every peer
+// (one NVLink traversal), then folds all N contributions in the same binomial order
+// and applies the update to its own copy.  No all-gather, no second hop; bit-identical
+// to the other variants because every rank evaluates the same expression.
+template <int N, class T>
+__global__ void __launch_bounds__(kThreads, 2) k_oneshot(XArgs a) {
+  constexpr int W = VecT<T>::W;
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  __shared__ uint32_t s_item;
+  __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
+  const int me = a.rank;
+  while (true) {
+    uint32_t it = claim(a.queue, &s_item) + a.item_begin;
+    if (it >= a.item_end) break;
+    if (N > 1 && it < a.push_items) {
+      constexpr int NP = N > 1 ? N - 1 : 1;
+      uint32_t c = it / NP;
+      int j = it % NP;
+      j += (j >= me);
+      uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
+      T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + lo);
+      uint64_t nvec = (hi - lo + W - 1) / W;
+      for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+        uint64_t e = lo + q * W;
+        int cnt = (int)min((uint64_t)W, hi - e);
+        T buf[W];
+        grad_vec<T>(a.g, e, cnt, buf);
+        st_vec<T>(dst + q * W, cnt, buf);
+      }
+      cta_release_flag(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
+    } else {
+      uint32_t c = it - a.push_items;
+      uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
+      if (threadIdx.x < N - 1) {
+        int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
+        s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)s * a.C + c;
+      }
+      __syncthreads();
+      cta_wait_flags(s_flags, N - 1, epoch, a.st);
+      const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + lo;
+      uint64_t nvec = (hi - lo + W - 1) / W;
+      for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += blockDim.x)
+        owner_vectors<N, T, 1, false>(a, rxb, lo, hi, q0, nvec);
+    }
+  }
+  retire(a.queue);
+}
+
 // ============================================================== TREE (paper)
 // Up: chunk c: acc = own + child_0 + child_1 + ... (children ascending, each the
 // child's subtree sum), then to the parent's rx slot, or on rank 0 the update
@@ -955,6 +1005,29 @@ void launch_twoshot(int N, bool tma, int want, int dev, cudaStream_t s, const XA
   }
 }
 
+template <int N, class T>
+int oneshot_grid(int want, int dev) {
+  static int cap[PGX_MAX_RANKS] = {};
+  if (!cap[dev]) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oneshot<N, T>, kThreads, 0);
+    cap[dev] = std::max(1, per_sm) * sm_count(dev);
+  }
+  return std::max(1, std::min(want, cap[dev]));
+}
+
+template <class T>
+void launch_oneshot(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n)                                                        \
+  case n:                                                                  \
+    k_oneshot<n, T><<<oneshot_grid<n, T>(want, dev), kThreads, 0, s>>>(a); \
+    break;
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
 template <class T>
 void launch_owner_local(int N, int grid, cudaStream_t s, const XArgs& a) {
   switch (N) {
@@ -1336,6 +1409,21 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0)) * own * x->esz +
                     (P.S - own) * x->esz;
 
+    } else if (P.variant == PGX_VARIANT_ONESHOT) {
+      P.sl = align_up(P.S, kAlignElems);  // slot stride: every peer's whole gradient
+      P.C = (uint32_t)((P.S + CH - 1) / CH);
+      P.K = N;
+      P.rx_off = rxoff;
+      rxoff = align_up(rxoff + 2 * (uint64_t)N * P.sl, kAlignElems);
+      P.rxflag_off = rxfoff;
+      rxfoff += (uint64_t)N * P.C;
+      P.push_items = (uint32_t)(N - 1) * P.C;
+      P.items = P.push_items + P.C;
+      P.expected = 0;  // each rank updates its own copy
+      P.grid = (int)std::min<uint64_t>(P.items, cap);
+      P.nvlink_bytes = (uint64_t)(N - 1) * P.S * x->esz;
+      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0)) * P.S * x->esz +
+                    (uint64_t)(N - 1) * P.S * x->esz;
     } else if (P.variant == PGX_VARIANT_TREE) {
       P.sl = align_up(P.S, kAlignElems);  // slot stride keeps every slot 16B-aligned
       P.C = (uint32_t)((P.S + CH - 1) / CH);
@@ -1511,6 +1599,24 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
   int prev;
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
+  if (P.variant == PGX_VARIANT_ONESHOT) {
+    xrecord(x->ready[l], s);
+    a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
+    a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
+    if (a.item_end > a.item_begin) {
+      ++x->launches;
+      int grid = (int)std::min<uint32_t>(a.item_end - a.item_begin, (uint32_t)P.grid);
+      if (x->esz == 8)
+        launch_oneshot<double>(x->world, grid, x->dev, s, a);
+      else
+        launch_oneshot<float>(x->world, grid, x->dev, s, a);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = xrecord(x->done[l], s);
+    if (prev != x->dev) cudaSetDevice(prev);
+    if (e != cudaSuccess) return fail(PGX_E_CUDA, "exchange launch failed: %s", cudaGetErrorString(e));
+    return PGX_OK;
+  }
   if (P.variant == PGX_VARIANT_NVLS) {
     xrecord(x->ready[l], s);
     int rc = launch_nvls(x, l, P, a, s);

@@ -24,18 +24,21 @@ from . import _lib
 from .errors import ConfigError, ShapeError
 
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
-            "nvls": _lib.VARIANT_NVLS}
+            "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32}
 
 
-def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20) -> str:
-    """Layer-size policy (measured, profiles/r1*_sweep*): small layers are latency-bound and
-    go through the SM two-shot kernel (fewest hops, ~26 us at 4 KB on 2 GPUs); layers of
-    `ce_from` elements or more move their shards with the copy engines, which do not take
-    SMs away from the backward kernels they overlap with.  `tree_below` optionally keeps
-    the paper's tree for the smallest layers."""
+def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20,
+                   oneshot_below: int = 1 << 16) -> str:
+    """Layer-size policy (measured, profiles/r1*_sweep*): the smallest layers are pure
+    latency and take the one-shot exchange (one NVLink hop); mid-size layers the SM
+    two-shot kernel; layers of `ce_from` elements or more move their shards with the copy
+    engines, which do not take SMs away from the backward kernels they overlap with.
+    `tree_below` optionally keeps the paper's tree for the smallest layers."""
     if world > 1 and elems < tree_below:
         return "tree"
+    if world > 1 and elems < oneshot_below:
+        return "oneshot"
     if world > 1 and elems >= ce_from:
         return "twoshot_ce"
     return "twoshot"

@@ -100,7 +100,8 @@ def _ngpu():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce") for m in ("ref32", "fast32")]
+@pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce", "oneshot")
+                                          for m in ("ref32", "fast32")]
                          + [("nvls", "fast32")])
 def test_concurrent_exchange_matches_oracle(variant, mode):
     out = _spawn(_exchange_worker, _ngpu(), variant, mode)
@@ -256,7 +257,7 @@ def _model_worker(rank, world, port, which, variant, gate, q):
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("which", ["lenet", "cifar10_quick"])
 @pytest.mark.parametrize("variant,gate", [("twoshot", "layer"), ("twoshot_ce", "layer"), ("tree", "layer"),
-                                          ("twoshot_ce", "model"), ("nvls", "layer")])
+                                          ("twoshot_ce", "model"), ("nvls", "layer"), ("oneshot", "layer")])
 def test_real_models_match_oracle(which, variant, gate):
     world = 2 if which == "lenet" else min(4, _ngpu())
     out = _spawn(_model_worker, world, which, variant, gate)
