@@ -29,12 +29,14 @@ MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE
 
 
 def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20,
-                   oneshot_below: int = 1 << 16) -> str:
+                   oneshot_below: int | None = None) -> str:
     """Layer-size policy (measured, profiles/r1*_sweep*): the smallest layers are pure
     latency and take the one-shot exchange (one NVLink hop); mid-size layers the SM
     two-shot kernel; layers of `ce_from` elements or more move their shards with the copy
     engines, which do not take SMs away from the backward kernels they overlap with.
     `tree_below` optionally keeps the paper's tree for the smallest layers."""
+    if oneshot_below is None:  # one-shot moves (N-1)*S per GPU: the crossover shrinks with N
+        oneshot_below = (1 << 20) // max(world, 1)  # N=4: 1 MB layers (profiles/r2b_sweep_n4)
     if world > 1 and elems < tree_below:
         return "tree"
     if world > 1 and elems < oneshot_below:
