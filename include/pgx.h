@@ -158,8 +158,11 @@ int pgx_seeded_fill_f32(uint64_t seed, double scale, float* out, uint64_t n, voi
  *                                  master update, broadcast down the same edges;
  *                        TWOSHOT = one-sided reduce-scatter to shard owners,
  *                                  owner fold (same tree order) + fused update,
- *                                  one-sided all-gather into peers' weights.
- * Both are bit-identical to the reference fold order. */
+ *                                  one-sided all-gather into peers' weights;
+ *                        ONESHOT = every rank pushes its whole gradient to every
+ *                                  peer and updates its own copy (small layers).
+ * TREE, TWOSHOT(_CE) and ONESHOT are bit-identical to the reference fold order;
+ * NVLS reduces in the switch (fast32, tolerance parity). */
 enum pgx_variant {
   PGX_VARIANT_TREE = 0,       /* paper: binomial reduce + master update + broadcast     */
   PGX_VARIANT_TWOSHOT = 1,    /* SM peer stores: reduce-scatter, owner update, gather   */
@@ -178,7 +181,8 @@ typedef struct pgx_xchg_config {
   uint64_t chunk_elems;          /* notification granularity, multiple of 4 */
   double lr;                     /* epsilon / learning rate */
   float scale, momentum, weight_decay;
-  uint32_t seg_base;             /* first of 3 segment ids used (model, rx, flags) */
+  uint32_t seg_base;             /* segment ids seg_base (weights + arrival flags) and
+                                    seg_base+1 (receive slots + their flags) */
   int max_ctas;                  /* CTAs per exchange launch (0 = auto) */
 } pgx_xchg_config;
 
