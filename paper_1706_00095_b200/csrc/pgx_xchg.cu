@@ -903,14 +903,14 @@ struct pgx_xchg {
   uint64_t launches = 0;
   cudaStream_t down = nullptr;
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
-  cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / reserved
-  int ce_parts = 4;                                // reduce-scatter / owner / all-gather pipelining depth
+  cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
+  int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
   bool tma = false;  // TWOSHOT: push / all-gather as TMA bulk copies (PGX_TMA=1; slower fused at N=4, profiles/r1r)
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
   std::vector<XEvent> rs_done, down_done;          // side-stream completion (joins for graph capture)
-  std::vector<XEvent> rs2_done, ce_own_done;
+  std::vector<XEvent> rs2_done;
   std::vector<std::vector<XEvent>> part_ev;        // TWOSHOT_CE owner parts ready for their all-gather
   uint32_t* iter_dev = nullptr;                    // device iteration counter (graph mode)
   bool device_iter = false;
@@ -1247,23 +1247,6 @@ static int launch_nvls(pgx_xchg* x, int l, const LayerPlan& P, const XArgs& a, c
 // TWOSHOT_CE launch: reduce-scatter and all-gather as peer DMA copies, each batch
 // followed (in stream order) by k_signal raising the peers' notifications with a
 // system-scope release; owner fold/update as a local kernel.
-// Parts of shard j: identical on every rank (a function of the shard length only), so
-// part p's reduce-scatter flag means the same range to the sender and to the owner.
-static int ce_num_parts(const pgx_xchg* x, const LayerPlan& P, uint64_t len) {
-  const uint64_t min_part = 1u << 18;  // elements: do not split small shards
-  int parts = x->world > 1 ? x->ce_parts : 1;
-  parts = std::min<int>(parts, (int)P.C);
-  while (parts > 1 && len / parts < min_part) --parts;
-  return std::max(parts, 1);
-}
-static uint64_t ce_part_lo(uint64_t lo, uint64_t len, int p, int parts) {
-  return p == 0 ? lo : lo + (len * p / parts) / 4 * 4;
-}
-
-// Copy-engine two-shot.  Push: part p of every peer's shard goes out as peer DMA copies,
-// then k_signal raises rxflag[me][p] on every owner.  Owner: part p waits for its N-1
-// flags, folds + updates it (k_owner_local), and its all-gather copies start while the
-// next part is folded — reduce-scatter, fold and all-gather overlap part by part.
 static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, cudaStream_t s, int phases) {
   const int N = x->world, me = x->rank;
   const int esz = x->esz;
@@ -1271,64 +1254,56 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
                  // all-gather, which the owner sends after reading the slot (per-layer forward gate)
   cudaError_t e = xrecord(x->ready[l], s);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
-  auto shard = [&](int j, uint64_t* lo, uint64_t* hi) {
-    *lo = std::min(P.S, (uint64_t)j * P.sl);
-    *hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
-  };
   if (phases & PGX_PHASE_PUSH) {
-    cudaStream_t cs = x->ce_rs;
-    xwait(cs, x->ready[l]);
-    int maxp = 1;
-    for (int j = 0; j < N; ++j) {
-      uint64_t lo, hi;
-      shard(j, &lo, &hi);
-      maxp = std::max(maxp, ce_num_parts(x, P, hi - lo));
-    }
-    for (int p = 0; p < maxp; ++p) {
-      FlagOut fo{};
-      for (int d = 1; d < N; ++d) {
-        int j = (me + d) % N;
-        uint64_t lo, hi;
-        shard(j, &lo, &hi);
-        int parts = ce_num_parts(x, P, hi - lo);
-        if (p >= parts) continue;
-        uint64_t plo = ce_part_lo(lo, hi - lo, p, parts), phi = p + 1 == parts ? hi : ce_part_lo(lo, hi - lo, p + 1, parts);
-        uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * P.sl + (plo - lo)) * esz;
-        uint64_t pb = 0;
-        for (int k = 0; k < a.g.n && plo < phi; ++k) {  // the part may straddle gradient pieces
-          uint64_t pe = a.g.end[k];
-          uint64_t ol = std::max(plo, pb), oh = std::min(phi, pe);
-          if (ol < oh) {
-            e = cudaMemcpyAsync(dst + (ol - plo) * esz, static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz,
-                                (oh - ol) * esz, cudaMemcpyDeviceToDevice, cs);
-            if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
-          }
-          pb = pe;
+    // peers alternate between one or two copy streams; each stream signals its own peers
+    const int ns = (x->ce_rs_streams > 1 && N > 2) ? 2 : 1;
+    cudaStream_t rs[2] = {x->ce_rs, x->ce_rs2};
+    FlagOut fo[2] = {};
+    for (int q = 0; q < ns; ++q) xwait(rs[q], x->ready[l]);
+    for (int d = 1; d < N; ++d) {
+      int j = (me + d) % N;
+      cudaStream_t cs = rs[(d - 1) % ns];
+      uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
+      uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * P.sl) * esz;
+      uint64_t pb = 0;
+      for (int k = 0; k < a.g.n && lo < hi; ++k) {
+        uint64_t pe = a.g.end[k];
+        uint64_t ol = std::max(lo, pb), oh = std::min(hi, pe);
+        if (ol < oh) {
+          e = cudaMemcpyAsync(dst + (ol - lo) * esz, static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz,
+                              (oh - ol) * esz, cudaMemcpyDeviceToDevice, cs);
+          if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
         }
-        fo.f[fo.n++] = a.rxflags[j] + (uint64_t)me * P.C + p;
+        pb = pe;
       }
-      if (fo.n) {
-        k_signal<<<1, 32, 0, cs>>>(fo, a.epoch, a.iter);
+      FlagOut& f = fo[(d - 1) % ns];
+      f.f[f.n++] = a.rxflags[j] + (uint64_t)me * P.C;
+    }
+    for (int q = 0; q < ns; ++q) {
+      if (fo[q].n) {
+        k_signal<<<1, 32, 0, rs[q]>>>(fo[q], a.epoch, a.iter);
         ++x->launches;
       }
+      xrecord(q == 0 ? x->rs_done[l] : x->rs2_done[l], rs[q]);
     }
-    xrecord(x->rs_done[l], cs);
   }
   if (phases & PGX_PHASE_OWNER) {
     xwait(x->ce_own, x->ready[l]);
-    xwait(x->ce_ag, x->ready[l]);  // keeps ce_ag joined even when there is nothing to copy
-    uint64_t lo, hi;
-    shard(me, &lo, &hi);
-    const int parts = ce_num_parts(x, P, hi - lo);
-    for (int p = 0; p < parts && lo < hi; ++p) {
-      uint64_t plo = ce_part_lo(lo, hi - lo, p, parts), phi = p + 1 == parts ? hi : ce_part_lo(lo, hi - lo, p + 1, parts);
-      FlagSet fs{};
-      for (int sidx = 0; sidx < N; ++sidx)
-        if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C + p;
-      if (fs.n) {
-        k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
-        ++x->launches;
-      }
+    FlagSet fs{};
+    fs.n = 0;
+    for (int sidx = 0; sidx < N; ++sidx)
+      if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C;
+    if (fs.n) {
+      k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
+      ++x->launches;
+    }
+    const uint64_t lo = std::min(P.S, (uint64_t)me * P.sl), hi = std::min(P.S, (uint64_t)(me + 1) * P.sl);
+    // owner fold/update in parts; each part's all-gather copies start as soon as it is done
+    int parts = N > 1 ? x->ce_parts : 1;
+    const uint64_t min_part = 1u << 18;  // elements: do not split small shards
+    while (parts > 1 && (hi - lo) / parts < min_part) --parts;
+    for (int p = 0; p < parts; ++p) {
+      uint64_t plo = lo + ((hi - lo) * p / parts) / 4 * 4, phi = p + 1 == parts ? hi : lo + ((hi - lo) * (p + 1) / parts) / 4 * 4;
       a.olo = plo;
       a.ohi = phi;
       int grid = std::max(1, std::min(P.grid, (int)(((phi - plo) / VecT<float>::W + kThreads - 1) / kThreads)));
@@ -1349,16 +1324,16 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
         if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
       }
     }
+    cudaStream_t tail = N > 1 ? x->ce_ag : x->ce_own;
+    if (N == 1 || lo >= hi) xwait(x->ce_ag, x->ready[l]);  // keep ce_ag joined even with nothing to copy
     FlagOut fo{};
     for (int d = 1; d < N; ++d)
       fo.f[fo.n++] = a.mflags[(me + d) % N] + x->ownerflag_base + (uint64_t)l * N + me;
     if (fo.n) {
-      k_signal<<<1, 32, 0, x->ce_ag>>>(fo, a.epoch, a.iter);
+      k_signal<<<1, 32, 0, tail>>>(fo, a.epoch, a.iter);
       ++x->launches;
     }
-    xrecord(x->ce_own_done[l], x->ce_own);
-    xwait(x->ce_ag, x->ce_own_done[l]);
-    e = xrecord(x->done[l], x->ce_ag);
+    e = xrecord(x->done[l], tail);
     if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
   }
   return PGX_OK;
@@ -1502,13 +1477,12 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_ag, cudaStreamNonBlocking, hi_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs2, cudaStreamNonBlocking, hi_prio);
     if (const char* v = getenv("PGX_CE_PARTS")) x->ce_parts = std::max(1, std::min(8, atoi(v)));
-
+    if (const char* v = getenv("PGX_CE_RS_STREAMS")) x->ce_rs_streams = std::max(1, std::min(2, atoi(v)));
     if (const char* v = getenv("PGX_TMA")) x->tma = atoi(v) != 0;
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
     x->rs_done.resize(cfg->num_layers);
     x->rs2_done.resize(cfg->num_layers);
-    x->ce_own_done.resize(cfg->num_layers);
     x->down_done.resize(cfg->num_layers);
     x->part_ev.resize(cfg->num_layers, std::vector<XEvent>(8));
     for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l) {
@@ -1517,7 +1491,6 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs_done[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->down_done[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs2_done[l].e, cudaEventDisableTiming);
-      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ce_own_done[l].e, cudaEventDisableTiming);
       for (int p = 0; p < 8 && e == cudaSuccess; ++p)
         e = cudaEventCreateWithFlags(&x->part_ev[l][p].e, cudaEventDisableTiming);
     }
@@ -1568,7 +1541,6 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   for (auto& e : x->rs_done) cudaEventDestroy(e.e);
   for (auto& e : x->down_done) cudaEventDestroy(e.e);
   for (auto& e : x->rs2_done) cudaEventDestroy(e.e);
-  for (auto& e : x->ce_own_done) cudaEventDestroy(e.e);
   for (auto& v : x->part_ev)
     for (auto& e : v) cudaEventDestroy(e.e);
   if (x->iter_dev) cudaFree(x->iter_dev);
