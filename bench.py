@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--gate", default="auto", choices=["auto", "layer", "model"],
                    help="per-layer forward gates, or one whole-model gate per step (auto: model if > 16 layers)")
     p.add_argument("--max-ctas", type=int, default=0)
+    p.add_argument("--low-priority-from", type=int, default=0,
+                   help="layers with at least this many elements launch on a normal-priority stream (0 = off)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager steps instead of a captured CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -244,7 +246,8 @@ def pgx_arm(args):
     sizes = [sum(p.numel() for p in ps) for _, ps in model.layers()]
     tr = DistTransport(rank, world, local, timeout_s=60.0)
     xchg = DeviceExchange(tr, sizes, mode="fast32", variant=args.variant, chunk_elems=args.chunk_elems,
-                          scale=1.0 / world, max_ctas=args.max_ctas, **wl["hyper"])
+                          scale=1.0 / world, max_ctas=args.max_ctas,
+                          low_priority_from=args.low_priority_from or None, **wl["hyper"])
     gate = args.gate if args.gate != "auto" else ("model" if len(sizes) > 16 else "layer")
     bind = ModuleBinding(xchg, model.layers(), gate=gate)
     if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)
@@ -437,6 +440,38 @@ def pgx_arm(args):
             by_layer.append({"layer": l, "bytes": n * 4, "variant": xchg.variants[l], "isolated_ms": ms_l,
                              "busbw_gbs": busbw, "frac_of_770": busbw / NVLINK_PEAK_GBS})
 
+    # the same large layers through the SM two-shot kernel (not the in-step choice at N>1 when
+    # the copy-engine variant is picked: SM stores are faster alone but steal SMs from cuDNN)
+    by_layer_sm = []
+    if world > 1 and by_layer and any(r["variant"] != "twoshot" for r in by_layer):
+        alt = DeviceExchange(tr, sizes, mode="fast32", variant="twoshot", chunk_elems=args.chunk_elems,
+                             scale=1.0 / world, seg_base=24, **wl["hyper"])
+        tr.sync_segments()
+        alt.connect()
+        for r in by_layer:
+            l, n = r["layer"], sizes[r["layer"]]
+            pieces = [torch.randn_like(p) * 1e-3 for p in model.layers()[l][1]]
+            ts = []
+            for i in range(12):
+                tr.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(alt.stream)
+                alt.launch(l, i, pieces)
+                alt.join(l, alt.stream)
+                alt.gate(l, i, stream=alt.stream)
+                e1.record(alt.stream)
+                torch.cuda.synchronize()
+                if i >= 2:
+                    ts.append(e0.elapsed_time(e1))
+            t = torch.tensor([statistics.median(ts)])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_l = float(t.item())
+            busbw = 2 * (world - 1) / world * n * 4 / (ms_l / 1e3) / 1e9
+            by_layer_sm.append({"layer": l, "bytes": n * 4, "variant": "twoshot", "isolated_ms": ms_l,
+                                "busbw_gbs": busbw, "frac_of_770": busbw / NVLINK_PEAK_GBS})
+        tr.barrier()
+        alt.close()
+
     nvl, hbm = xchg.layer_bytes(L_DOM)
     avg = statistics.mean(durs) if durs else None
     kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local + copy-engine transfers",
@@ -475,7 +510,7 @@ def pgx_arm(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
             "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None, "timeline": timeline,
-            "exchange_by_layer": by_layer or None}
+            "exchange_by_layer": by_layer or None, "exchange_by_layer_sm_twoshot": by_layer_sm or None}
     if args.per_gpu_batch:
         line["config"]["per_gpu_batch"] = B
         line["config"]["global_batch"] = gb

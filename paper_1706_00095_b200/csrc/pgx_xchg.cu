@@ -905,6 +905,7 @@ struct pgx_xchg {
   cudaStream_t ce_rs = nullptr, ce_own = nullptr;  // TWOSHOT_CE: push copies / owner side
   cudaStream_t ce_ag = nullptr, ce_rs2 = nullptr;  // TWOSHOT_CE: all-gather copies / 2nd push stream
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
+  bool ce_rs_parts = false;                        // push signals per owner part (signals on ce_rs2)
   bool tma = false;  // TWOSHOT: push / all-gather as TMA bulk copies (PGX_TMA=1; slower fused at N=4, profiles/r1r)
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
@@ -912,6 +913,7 @@ struct pgx_xchg {
   std::vector<XEvent> rs_done, down_done;          // side-stream completion (joins for graph capture)
   std::vector<XEvent> rs2_done;
   std::vector<std::vector<XEvent>> part_ev;        // TWOSHOT_CE owner parts ready for their all-gather
+  std::vector<std::vector<XEvent>> rs_part_ev;     // TWOSHOT_CE push parts copied (per-part signals)
   uint32_t* iter_dev = nullptr;                    // device iteration counter (graph mode)
   bool device_iter = false;
   uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
@@ -1244,6 +1246,22 @@ static int launch_nvls(pgx_xchg* x, int l, const LayerPlan& P, const XArgs& a, c
   return PGX_OK;
 }
 
+// TWOSHOT_CE: owner j's shard split into its pipelined parts (the same split on the
+// pushing and the owning side); returns the part count and part p's [lo, hi).
+static int ce_split(const pgx_xchg* x, const LayerPlan& P, int j, int p, uint64_t* plo, uint64_t* phi) {
+  const uint64_t lo = std::min(P.S, (uint64_t)j * P.sl), hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
+  int parts = x->world > 1 ? x->ce_parts : 1;
+  const uint64_t min_part = 1u << 18;  // elements: do not split small shards
+  while (parts > 1 && (hi - lo) / parts < min_part) --parts;
+  parts = std::min<int>(parts, (int)P.C);
+  if (parts < 1) parts = 1;
+  if (plo) {
+    *plo = lo + ((hi - lo) * p / parts) / 4 * 4;
+    *phi = p + 1 == parts ? hi : lo + ((hi - lo) * (p + 1) / parts) / 4 * 4;
+  }
+  return parts;
+}
+
 // TWOSHOT_CE launch: reduce-scatter and all-gather as peer DMA copies, each batch
 // followed (in stream order) by k_signal raising the peers' notifications with a
 // system-scope release; owner fold/update as a local kernel.
@@ -1254,7 +1272,45 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
                  // all-gather, which the owner sends after reading the slot (per-layer forward gate)
   cudaError_t e = xrecord(x->ready[l], s);
   if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
-  if (phases & PGX_PHASE_PUSH) {
+  const bool rs_parts = x->ce_rs_parts && N > 1;
+  if ((phases & PGX_PHASE_PUSH) && rs_parts) {
+    // part-major push: all peers' part p, then an event; the signals for part p run on
+    // ce_rs2 behind that event, so the copy queue never drains waiting for a kernel and
+    // each owner starts folding part p while part p+1 is still in flight
+    xwait(x->ce_rs, x->ready[l]);
+    xwait(x->ce_rs2, x->ready[l]);
+    int np[PGX_MAX_RANKS] = {}, pmax = 0;
+    for (int j = 0; j < N; ++j) pmax = std::max(pmax, np[j] = ce_split(x, P, j, 0, nullptr, nullptr));
+    for (int p = 0; p < pmax; ++p) {
+      FlagOut fo{};
+      for (int d = 1; d < N; ++d) {
+        int j = (me + d) % N;
+        if (p >= np[j]) continue;
+        uint64_t lo, hi, jlo = std::min(P.S, (uint64_t)j * P.sl);
+        ce_split(x, P, j, p, &lo, &hi);
+        uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)(a.parity * a.K + me) * P.sl + (lo - jlo)) * esz;
+        uint64_t pb = 0;
+        for (int k = 0; k < a.g.n && lo < hi; ++k) {
+          uint64_t pe = a.g.end[k];
+          uint64_t ol = std::max(lo, pb), oh = std::min(hi, pe);
+          if (ol < oh) {
+            e = cudaMemcpyAsync(dst + (ol - lo) * esz, static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz,
+                                (oh - ol) * esz, cudaMemcpyDeviceToDevice, x->ce_rs);
+            if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
+          }
+          pb = pe;
+        }
+        fo.f[fo.n++] = a.rxflags[j] + (uint64_t)me * P.C + p;
+      }
+      if (!fo.n) continue;
+      xrecord(x->rs_part_ev[l][p], x->ce_rs);
+      xwait(x->ce_rs2, x->rs_part_ev[l][p]);
+      k_signal<<<1, 32, 0, x->ce_rs2>>>(fo, a.epoch, a.iter);
+      ++x->launches;
+    }
+    xrecord(x->rs_done[l], x->ce_rs);
+    xrecord(x->rs2_done[l], x->ce_rs2);
+  } else if (phases & PGX_PHASE_PUSH) {
     // peers alternate between one or two copy streams; each stream signals its own peers
     const int ns = (x->ce_rs_streams > 1 && N > 2) ? 2 : 1;
     cudaStream_t rs[2] = {x->ce_rs, x->ce_rs2};
@@ -1289,21 +1345,21 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
   }
   if (phases & PGX_PHASE_OWNER) {
     xwait(x->ce_own, x->ready[l]);
-    FlagSet fs{};
-    fs.n = 0;
-    for (int sidx = 0; sidx < N; ++sidx)
-      if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C;
-    if (fs.n) {
-      k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
-      ++x->launches;
-    }
     const uint64_t lo = std::min(P.S, (uint64_t)me * P.sl), hi = std::min(P.S, (uint64_t)(me + 1) * P.sl);
     // owner fold/update in parts; each part's all-gather copies start as soon as it is done
-    int parts = N > 1 ? x->ce_parts : 1;
-    const uint64_t min_part = 1u << 18;  // elements: do not split small shards
-    while (parts > 1 && (hi - lo) / parts < min_part) --parts;
+    const int parts = ce_split(x, P, me, 0, nullptr, nullptr);
     for (int p = 0; p < parts; ++p) {
-      uint64_t plo = lo + ((hi - lo) * p / parts) / 4 * 4, phi = p + 1 == parts ? hi : lo + ((hi - lo) * (p + 1) / parts) / 4 * 4;
+      if (p == 0 || rs_parts) {  // whole-shard signal, or this part's signal from every peer
+        FlagSet fs{};
+        for (int sidx = 0; sidx < N; ++sidx)
+          if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C + (rs_parts ? p : 0);
+        if (fs.n) {
+          k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
+          ++x->launches;
+        }
+      }
+      uint64_t plo, phi;
+      ce_split(x, P, me, p, &plo, &phi);
       a.olo = plo;
       a.ohi = phi;
       int grid = std::max(1, std::min(P.grid, (int)(((phi - plo) / VecT<float>::W + kThreads - 1) / kThreads)));
@@ -1478,6 +1534,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs2, cudaStreamNonBlocking, hi_prio);
     if (const char* v = getenv("PGX_CE_PARTS")) x->ce_parts = std::max(1, std::min(8, atoi(v)));
     if (const char* v = getenv("PGX_CE_RS_STREAMS")) x->ce_rs_streams = std::max(1, std::min(2, atoi(v)));
+    if (const char* v = getenv("PGX_CE_RS_PARTS")) x->ce_rs_parts = atoi(v) != 0;
     if (const char* v = getenv("PGX_TMA")) x->tma = atoi(v) != 0;
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
@@ -1485,14 +1542,17 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     x->rs2_done.resize(cfg->num_layers);
     x->down_done.resize(cfg->num_layers);
     x->part_ev.resize(cfg->num_layers, std::vector<XEvent>(8));
+    x->rs_part_ev.resize(cfg->num_layers, std::vector<XEvent>(8));
     for (int l = 0; l < cfg->num_layers && e == cudaSuccess; ++l) {
       e = cudaEventCreateWithFlags(&x->done[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->ready[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs_done[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->down_done[l].e, cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs2_done[l].e, cudaEventDisableTiming);
-      for (int p = 0; p < 8 && e == cudaSuccess; ++p)
+      for (int p = 0; p < 8 && e == cudaSuccess; ++p) {
         e = cudaEventCreateWithFlags(&x->part_ev[l][p].e, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x->rs_part_ev[l][p].e, cudaEventDisableTiming);
+      }
     }
     if (e == cudaSuccess) e = cudaMalloc(&x->iter_dev, sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(x->iter_dev, 0xFF, sizeof(uint32_t));
@@ -1542,6 +1602,8 @@ int pgx_xchg_destroy(pgx_xchg* x) {
   for (auto& e : x->down_done) cudaEventDestroy(e.e);
   for (auto& e : x->rs2_done) cudaEventDestroy(e.e);
   for (auto& v : x->part_ev)
+    for (auto& e : v) cudaEventDestroy(e.e);
+  for (auto& v : x->rs_part_ev)
     for (auto& e : v) cudaEventDestroy(e.e);
   if (x->iter_dev) cudaFree(x->iter_dev);
   if (x->gate_table) cudaFree(x->gate_table);

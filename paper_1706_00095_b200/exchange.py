@@ -50,7 +50,7 @@ class DeviceExchange:
     def __init__(self, transport, layer_elems, *, mode: str = "fast32", variant="twoshot",
                  chunk_elems: int = 16384, lr: float = 0.01, scale: float | None = None,
                  momentum: float = 0.0, weight_decay: float = 0.0, seg_base: int = 16, max_ctas: int = 0,
-                 tree_below: int = 0):
+                 tree_below: int = 0, low_priority_from: int | None = None):
         if mode not in MODES:
             raise ConfigError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
         self.tr = transport
@@ -98,6 +98,10 @@ class DeviceExchange:
         self.layer_views = [self.model[o:o + n] for o, n in zip(self.model_offsets, self.layer_elems)]
         with torch.cuda.device(transport.device):
             self.stream = torch.cuda.Stream(device=transport.device, priority=-1)
+            # optional: large layers (long slack before their next use) launch at normal priority
+            # so their CTAs fill gaps instead of pre-empting the backward kernels
+            self.stream_low = torch.cuda.Stream(device=transport.device, priority=0)
+        self.low_priority_from = low_priority_from
         self.connected = False
         self.device_iteration = False
         self.launches = 0
@@ -160,6 +164,12 @@ class DeviceExchange:
         return nvl.value, hbm.value
 
     # -- per-layer operations ------------------------------------------------------
+    def stream_for(self, layer: int):
+        """The launch stream of a layer (high priority unless it is a large, slack-rich layer)."""
+        if self.low_priority_from is not None and self.layer_elems[layer] >= self.low_priority_from:
+            return self.stream_low
+        return self.stream
+
     def launch(self, layer: int, iteration: int, pieces, stream=None, phases: int = _lib.PHASE_ALL) -> None:
         """Exchange layer `layer` of iteration `iteration`; `pieces` are device tensors
         covering the layer's flat gradient in order (e.g. [dW, db])."""
@@ -173,7 +183,7 @@ class DeviceExchange:
                 raise ShapeError("gradient pieces must be contiguous")
         ptrs = (C.c_void_p * n)(*[p.data_ptr() for p in pieces])
         cnts = (C.c_uint64 * n)(*[p.numel() for p in pieces])
-        st = stream or self.stream
+        st = stream or self.stream_for(layer)
         _lib.call("pgx_xchg_layer", self.handle, layer, iteration & 0xFFFFFFFF, ptrs, cnts, n, phases, st.cuda_stream)
         if not torch.cuda.is_current_stream_capturing():
             # the pieces are read asynchronously on the launch stream and, for the copy-engine
@@ -285,7 +295,8 @@ class ModuleBinding:
                 return
             self._pending[l] = 0
             compute = torch.cuda.current_stream(self.x.tr.device)
-            self.x.stream.wait_stream(compute)
+            xs = self.x.stream_for(l)
+            xs.wait_stream(compute)
             pieces = []
             for p in params:
                 g = p.grad
@@ -300,8 +311,8 @@ class ModuleBinding:
                 ext = torch.cuda.is_current_stream_capturing()
                 e0 = torch.cuda.Event(enable_timing=True, external=ext)
                 e1 = torch.cuda.Event(enable_timing=True, external=ext)
-                e0.record(self.x.stream)
-            self.x.launch(l, self.k, pieces)
+                e0.record(xs)
+            self.x.launch(l, self.k, pieces, stream=xs)
             if timed:  # end = this rank's part done on every internal stream (copy-engine variants too)
                 if self._tstream is None:
                     self._tstream = torch.cuda.Stream(device=self.x.tr.device)

@@ -412,7 +412,8 @@ class DistTransport(CudaTransport):
         from .rendezvous import exchange
 
         mine = {}
-        for sid in sorted(list(self._segments) + [CONTROL_SEGMENT]):
+        shared = getattr(self, "_shared", set())
+        for sid in sorted(set(list(self._segments) + [CONTROL_SEGMENT]) - shared):
             buf = (C.c_uint8 * _lib.IPC_HANDLE_BYTES)()
             _lib.call("pgx_segment_export", self.handle, sid, buf)
             d, f, sz, cnt = C.c_void_p(), C.c_void_p(), C.c_uint64(), C.c_uint32()
@@ -426,7 +427,13 @@ class DistTransport(CudaTransport):
             for sid, (handle, size, count) in segs.items():
                 hb = (C.c_uint8 * _lib.IPC_HANDLE_BYTES).from_buffer_copy(handle)
                 _lib.call("pgx_segment_attach_ipc", self.handle, peer, sid, hb, size, count)
+        self._shared = shared | set(mine)
         self._connected = True
+
+    def sync_segments(self) -> None:
+        """Collective: attach the segments every rank created after the first rendezvous
+        (e.g. a second exchange object); already-attached ones are not exchanged again."""
+        self.connect()
 
     def _ensure_connected(self, rank: int) -> None:
         if not self._connected and rank != self.rank:

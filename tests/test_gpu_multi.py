@@ -19,7 +19,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _exchange_worker(rank, world, port, variant, mode, q):
+def _exchange_worker(rank, world, port, variant, mode, late, q):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -31,6 +31,8 @@ def _exchange_worker(rank, world, port, variant, mode, q):
 
     try:
         tr = DistTransport(rank, world, rank, timeout_s=20.0)
+        if late:  # rendezvous first; the exchange's segments are attached afterwards
+            tr.barrier()
         elems = LENET + [1 << 20]
         hyper = dict(lr=0.01, momentum=0.9, weight_decay=5e-4) if mode == "fast32" else dict(lr=0.05)
         x = DeviceExchange(tr, elems, mode=mode, variant=variant, chunk_elems=16384, **hyper)
@@ -40,6 +42,8 @@ def _exchange_worker(rank, world, port, variant, mode, q):
         for l in range(len(elems)):
             x.layer_views[l].copy_(torch.from_numpy(w[l]))
         torch.cuda.synchronize()
+        if late:
+            tr.sync_segments()
         tr.barrier()  # rendezvous: IPC handles exchanged, peers attached
         x.connect()
         comp = torch.cuda.current_stream()
@@ -104,7 +108,16 @@ def _ngpu():
                                           for m in ("ref32", "fast32")]
                          + [("nvls", "fast32")])
 def test_concurrent_exchange_matches_oracle(variant, mode):
-    out = _spawn(_exchange_worker, _ngpu(), variant, mode)
+    out = _spawn(_exchange_worker, _ngpu(), variant, mode, False)
+    for rank, bad, status in out:
+        assert bad == [] and status == 0, (rank, bad, status)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce"])
+def test_exchange_created_after_rendezvous(variant):
+    """DistTransport.sync_segments attaches segments created after the first barrier."""
+    out = _spawn(_exchange_worker, _ngpu(), variant, "fast32", True)
     for rank, bad, status in out:
         assert bad == [] and status == 0, (rank, bad, status)
 
