@@ -49,12 +49,16 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "nvls", "oneshot", "auto", "nccl_bulk", "ddp"],
+    p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "twoshot_cep", "nvls", "oneshot", "auto", "nccl_bulk", "ddp"],
                    help="nccl_bulk / ddp are comparison rows (NCCL on the path), not the product")
     p.add_argument("--chunk-elems", type=int, default=16384)
     p.add_argument("--gate", default="auto", choices=["auto", "layer", "model"],
                    help="per-layer forward gates, or one whole-model gate per step (auto: model if > 16 layers)")
     p.add_argument("--max-ctas", type=int, default=0)
+    p.add_argument("--large", choices=("ce", "cep", "sm"), default="ce",
+                   help="auto policy for layers >= 1M elements: copy-engine or SM two-shot")
+    p.add_argument("--large-ctas", type=int, default=0, help="CTA cap of the large layers' launches (0 = auto)")
+    p.add_argument("--large-chunk-elems", type=int, default=0, help="chunk of the large layers (0 = --chunk-elems)")
     p.add_argument("--low-priority-from", type=int, default=0,
                    help="layers with at least this many elements launch on a normal-priority stream (0 = off)")
     p.add_argument("--no-e2e", action="store_true")
@@ -160,7 +164,9 @@ def workload_config(world, args):
             "parallelism": f"dp{world}", "exchange": args.variant, "update": f"fast32 momentum SGD lr {h['lr']} mu {h['momentum']} "
             f"wd {h['weight_decay']} scale 1/N", "fwd_bwd": "PyTorch cuDNN bf16 autocast, fp32 master weights/grads",
             "l2": "working set > L2 (244 MB fp32 weights + 244 MB grads + activations per step)",
-            "chunk_elems": args.chunk_elems, "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager"}
+            "chunk_elems": args.chunk_elems, "large_layers": {"variant": args.large, "ctas": args.large_ctas,
+                                                               "chunk_elems": args.large_chunk_elems},
+            "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager"}
 
 
 # ------------------------------------------------------------------ model
@@ -247,7 +253,8 @@ def pgx_arm(args):
     tr = DistTransport(rank, world, local, timeout_s=60.0)
     xchg = DeviceExchange(tr, sizes, mode="fast32", variant=args.variant, chunk_elems=args.chunk_elems,
                           scale=1.0 / world, max_ctas=args.max_ctas,
-                          low_priority_from=args.low_priority_from or None, **wl["hyper"])
+                          low_priority_from=args.low_priority_from or None, large=args.large,
+                          large_ctas=args.large_ctas, large_chunk_elems=args.large_chunk_elems, **wl["hyper"])
     gate = args.gate if args.gate != "auto" else ("model" if len(sizes) > 16 else "layer")
     bind = ModuleBinding(xchg, model.layers(), gate=gate)
     if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)
@@ -389,7 +396,7 @@ def pgx_arm(args):
     # recorded by every eager step) bracket that layer's exchange on its streams ----
     durs = []
     if graph is not None:
-        for _ in range(5):  # a few more replays, each read back (the captured events hold the last one)
+        for _ in range(9):  # a few more replays, each read back (the captured events hold the last one)
             run_step()
             torch.cuda.synchronize()
             a, b_ = bind.events[L_DOM][0]
@@ -445,7 +452,7 @@ def pgx_arm(args):
     by_layer_sm = []
     if world > 1 and by_layer and any(r["variant"] != "twoshot" for r in by_layer):
         alt = DeviceExchange(tr, sizes, mode="fast32", variant="twoshot", chunk_elems=args.chunk_elems,
-                             scale=1.0 / world, seg_base=24, **wl["hyper"])
+                             scale=1.0 / world, seg_base=24, large_chunk_elems=65536, **wl["hyper"])
         tr.sync_segments()
         alt.connect()
         for r in by_layer:
@@ -467,19 +474,21 @@ def pgx_arm(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_l = float(t.item())
             busbw = 2 * (world - 1) / world * n * 4 / (ms_l / 1e3) / 1e9
-            by_layer_sm.append({"layer": l, "bytes": n * 4, "variant": "twoshot", "isolated_ms": ms_l,
+            by_layer_sm.append({"layer": l, "bytes": n * 4, "variant": "twoshot", "chunk_elems": alt.layer_chunk_elems[l],
+                                "isolated_ms": ms_l,
                                 "busbw_gbs": busbw, "frac_of_770": busbw / NVLINK_PEAK_GBS})
         tr.barrier()
         alt.close()
 
     nvl, hbm = xchg.layer_bytes(L_DOM)
-    avg = statistics.mean(durs) if durs else None
+    avg = statistics.median(durs) if durs else None  # median: one replay can catch a host hiccup
     kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local + copy-engine transfers",
+             "twoshot_cep": "k_twoshot owner items + copy-engine reduce-scatter",
              "tree": "k_tree_up/k_tree_down", "nvls": "k_nvls (multimem)",
              "oneshot": "k_oneshot"}[xchg.variants[L_DOM]]
     what = "%s, layer %d (%d params): fold + fused momentum update%s" % (
         kname, L_DOM, sizes[L_DOM], " + reduce-scatter/all-gather over NVLink" if world > 1 else "")
-    measured_in = (("CUDA events captured in the step graph, %d replays after the timed region" % len(durs))
+    measured_in = (("median of CUDA events captured in the step graph, %d replays after the timed region" % len(durs))
                    if graph is not None else "CUDA events in every timed eager step")
     traffic = ncu_traffic(kname.split()[0], world, sizes[L_DOM])
     roof = None
@@ -487,7 +496,7 @@ def pgx_arm(args):
         peak, peak_src = hbm_peak()
         ach = hbm / (avg / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": what, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": traffic, "algorithmic_bytes_per_launch": hbm, "avg_launch_ms_in_step": avg,
+                "traffic": traffic, "algorithmic_bytes_per_launch": hbm, "avg_launch_ms_in_step": avg, "in_step_ms_samples": [round(d, 4) for d in durs],
                 "peak_source": peak_src, "launch_share_of_step": avg / (ms / args.steps), "measured_in": measured_in}
         if iso:
             roof["isolated_launch_ms"] = statistics.median(iso)
@@ -499,7 +508,7 @@ def pgx_arm(args):
         roof = {"bound": "nvlink", "kernel": what, "achieved": ach, "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                 "frac": ach / NVLINK_PEAK_GBS, "traffic": traffic, "algorithmic_bytes_per_launch": nvl,
                 "bytes": "2(N-1)/N x layer bytes leave this GPU (reduce-scatter + all-gather)",
-                "avg_launch_ms_in_step": avg, "launch_share_of_step": avg / (ms / args.steps),
+                "avg_launch_ms_in_step": avg, "in_step_ms_samples": [round(d, 4) for d in durs], "launch_share_of_step": avg / (ms / args.steps),
                 "peak_source": "B200_PROFILING.md measured NVLink peer copy per direction (900 nominal)",
                 "measured_in": measured_in + "; in-step time includes waiting for the slowest rank's gradient",
                 "isolated_ms": iso_ms, "isolated_achieved": nvl / (iso_ms / 1e3) / 1e9,
@@ -567,7 +576,7 @@ def trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world, steps=3):
     path = args.timeline or ""
     if path:
         write_timeline_csv(rec.events, path.replace("{rank}", str(rank)))
-    return {"overlap_ratio": compute_overlap(rec.events), "steps_traced": steps,
+    return {"overlap_ratio": compute_overlap(rec.events).overlap_ratio, "steps_traced": steps,
             "exchange_tail_after_backward_ms": statistics.mean(tails), "schema": "timeline.py:34 CSV",
             "csv": path or None}
 

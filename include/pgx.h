@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 1
+#define PGX_ABI_VERSION 2
 #define PGX_IPC_HANDLE_BYTES 64
 #define PGX_CONTROL_SEGMENT 15 /* transport/base.py:21 */
 #define PGX_MAX_RANKS 8
@@ -37,7 +37,8 @@ enum pgx_status {
   PGX_E_TRANSPORT = 7, /* TransportError  errors.py:32 */
   PGX_E_PROTOCOL = 8,  /* ProtocolError   errors.py:36 */
   PGX_E_TIMEOUT = 9,   /* TransportError (bounded device/host wait expired) */
-  PGX_E_CUDA = 10      /* TransportError (CUDA runtime failure) */
+  PGX_E_CUDA = 10,     /* TransportError (CUDA runtime failure) */
+  PGX_E_FORMAT = 11    /* FormatError     errors.py:49 */
 };
 
 typedef struct pgx_world pgx_world;
@@ -145,6 +146,27 @@ enum pgx_mode {
 int pgx_fold_update(int mode, const void* const* partials, int world, void* w, float* v,
                     uint64_t n, double eps, float scale, float momentum, float weight_decay,
                     void* stream);
+/* ------------------------------------------------------------------ checkpoints
+ * PSGD1 model checkpoints (engine/checkpoint.py:1-71): "PSGD1", then per layer
+ * u32 index, u64 count, count x f64 (little-endian).  Replaces serialize_model
+ * (:29-39) and load_model_bytes (:42-63): the image is built / read by one device
+ * kernel from / into the layers (fp32 layers are promoted exactly / rounded to
+ * nearest); header validation is host code with the reference's FormatError
+ * messages. */
+#define PGX_CKPT_MAX_LAYERS 512
+/* image bytes = 5 + sum(12 + 8*count) */
+int pgx_ckpt_image_bytes(const uint64_t* counts, int num_layers, uint64_t* bytes_out);
+/* Host: walk and validate a PSGD1 blob (load_model_bytes, checkpoint.py:42-63);
+ * counts_out may be NULL (count only).  PGX_E_FORMAT with the reference messages. */
+int pgx_ckpt_parse(const void* blob, uint64_t bytes, uint64_t* counts_out, int capacity, int* num_layers_out);
+/* Device: layers (elem_size 4 or 8) -> image (8-byte aligned, capacity >= bytes
+ * rounded up to 8; the pad bytes are zero). */
+int pgx_ckpt_pack(const void* const* layers, const uint64_t* counts, int num_layers, int elem_size, void* image,
+                  uint64_t capacity, void* stream);
+/* Device: image (8-byte aligned, capacity >= bytes rounded up to 8, plus 8) -> layers. */
+int pgx_ckpt_unpack(const void* image, uint64_t capacity, const uint64_t* counts, int num_layers, int elem_size,
+                    void* const* layers, void* stream);
+
 /* seeded_fill (buffers.py:54-66) on the device, bit-identical to numpy. */
 int pgx_seeded_fill_f64(uint64_t seed, double scale, double* out, uint64_t n, void* stream);
 int pgx_seeded_fill_f32(uint64_t seed, double scale, float* out, uint64_t n, void* stream);
@@ -161,7 +183,7 @@ int pgx_seeded_fill_f32(uint64_t seed, double scale, float* out, uint64_t n, voi
  *                                  one-sided all-gather into peers' weights;
  *                        ONESHOT = every rank pushes its whole gradient to every
  *                                  peer and updates its own copy (small layers).
- * TREE, TWOSHOT(_CE) and ONESHOT are bit-identical to the reference fold order;
+ * TREE, TWOSHOT(_CE/_CEP) and ONESHOT are bit-identical to the reference fold order;
  * NVLS reduces in the switch (fast32, tolerance parity). */
 enum pgx_variant {
   PGX_VARIANT_TREE = 0,       /* paper: binomial reduce + master update + broadcast     */
@@ -169,8 +191,11 @@ enum pgx_variant {
   PGX_VARIANT_TWOSHOT_CE = 2, /* same schedule, shards moved by the copy engines        */
   PGX_VARIANT_NVLS = 3,       /* NVLink SHARP: in-switch reduce (multimem.ld_reduce) +
                                  multicast weight store; fast32 only, tolerance parity  */
-  PGX_VARIANT_ONESHOT = 4     /* small layers: everyone pushes everything once, every
+  PGX_VARIANT_ONESHOT = 4,    /* small layers: everyone pushes everything once, every
                                  rank folds (same order) and updates its own copy       */
+  PGX_VARIANT_TWOSHOT_CEP = 5 /* reduce-scatter by the copy engines, then the SM owner
+                                 kernel (fold + update + all-gather peer stores) on a
+                                 capped grid: no per-part copy/event chain            */
 };
 
 typedef struct pgx_xchg_config {
@@ -184,6 +209,8 @@ typedef struct pgx_xchg_config {
   uint32_t seg_base;             /* segment ids seg_base (weights + arrival flags) and
                                     seg_base+1 (receive slots + their flags) */
   int max_ctas;                  /* CTAs per exchange launch (0 = auto) */
+  const uint64_t* layer_chunk_elems; /* optional per-layer chunk_elems (NULL or 0 = chunk_elems) */
+  const int* layer_max_ctas;     /* optional per-layer CTA cap (NULL or 0 = max_ctas) */
 } pgx_xchg_config;
 
 int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out);

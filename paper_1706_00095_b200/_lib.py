@@ -22,9 +22,11 @@ CONTROL_SEGMENT = 15
 MAX_RANKS = 8
 MAX_PIECES = 4
 XCHG_STREAMS = 5
+CKPT_MAX_LAYERS = 512
 
 MODE_REF64, MODE_REF32, MODE_FAST32 = 0, 1, 2
 VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE, VARIANT_NVLS, VARIANT_ONESHOT = 0, 1, 2, 3, 4
+VARIANT_TWOSHOT_CEP = 5
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p
@@ -45,6 +47,8 @@ class XchgConfig(C.Structure):
         ("weight_decay", C.c_float),
         ("seg_base", u32),
         ("max_ctas", i32),
+        ("layer_chunk_elems", P(u64)),
+        ("layer_max_ctas", P(i32)),
     ]
 
 
@@ -79,6 +83,10 @@ SIGNATURES = {
     "pgx_tree_reduce_f64": [P(vp), i32, vp, u64, vp],
     "pgx_tree_reduce_f32": [P(vp), i32, vp, u64, vp],
     "pgx_fold_update": [i32, P(vp), i32, vp, vp, u64, C.c_double, C.c_float, C.c_float, C.c_float, vp],
+    "pgx_ckpt_image_bytes": [P(u64), i32, P(u64)],
+    "pgx_ckpt_parse": [vp, u64, P(u64), i32, P(i32)],
+    "pgx_ckpt_pack": [P(vp), P(u64), i32, i32, vp, u64, vp],
+    "pgx_ckpt_unpack": [vp, u64, P(u64), i32, i32, P(vp), vp],
     "pgx_seeded_fill_f64": [u64, C.c_double, vp, u64, vp],
     "pgx_seeded_fill_f32": [u64, C.c_double, vp, u64, vp],
     "pgx_xchg_create": [vp, P(XchgConfig), P(vp)],

@@ -1,0 +1,237 @@
+// PSGD1 model checkpoints (engine/checkpoint.py:1-71) built and read on the device.
+//
+// Image (little-endian): "PSGD1", then per layer l: u32 l, u64 count, count x f64.
+// Layer l's header starts at off[l] = 5 + sum_{i<l} (12 + 8 n_i), so every value
+// sits at an odd byte offset: the pack kernel assembles each ALIGNED 8-byte output
+// word from the two values it straddles (one funnel shift) and writes it with one
+// 64-bit store, so a launch is a single coalesced HBM stream (read n*esz, write
+// 8n bytes); only words touching a header or the magic are built byte by byte.
+// Unpack is the mirror: each value is read from its two aligned image words.
+// fp32 layers are promoted exactly to f64 on the way out (the reference
+// serializes np.asarray(values, "<f8")) and rounded to nearest on the way in.
+// Header validation (pgx_ckpt_parse) is host code over the file bytes, with the
+// reference's FormatError messages.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <memory>
+#include <string>
+
+#include "pgx_common.cuh"
+
+using namespace pgx;
+
+namespace {
+
+constexpr int kMaxLayers = PGX_CKPT_MAX_LAYERS;
+constexpr int kThreads = 256;
+
+struct CkptTable {                // kernel parameter (< 32 KB)
+  const void* p[kMaxLayers];      // layer data: source (pack) or destination (unpack)
+  uint64_t off[kMaxLayers + 1];   // byte offset of layer l's header; off[L] = image bytes
+  uint64_t cum[kMaxLayers + 1];   // cumulative element counts
+  int L;
+  int esz;
+};
+
+__device__ __forceinline__ int find_layer(const uint64_t* a, int L, uint64_t x) {
+  // largest l in [0, L) with a[l] <= x (a ascending, a[0] <= x)
+  int lo = 0, hi = L - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (a[mid] <= x)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint64_t value_bits(const CkptTable& t, int l, uint64_t k) {
+  if (t.esz == 8) return (uint64_t)__double_as_longlong(static_cast<const double*>(t.p[l])[k]);
+  return (uint64_t)__double_as_longlong((double)static_cast<const float*>(t.p[l])[k]);
+}
+
+__device__ uint8_t image_byte(const CkptTable& t, uint64_t pos) {
+  if (pos < 5) return (uint8_t)("PSGD1"[pos]);
+  int l = find_layer(t.off, t.L, pos);
+  uint64_t r = pos - t.off[l];
+  if (r < 4) return (uint8_t)((uint32_t)l >> (8 * r));
+  if (r < 12) return (uint8_t)((t.cum[l + 1] - t.cum[l]) >> (8 * (r - 4)));
+  r -= 12;
+  return (uint8_t)(value_bits(t, l, r >> 3) >> (8 * (r & 7)));
+}
+
+__global__ void __launch_bounds__(kThreads) k_ckpt_pack(const __grid_constant__ CkptTable t, uint64_t* __restrict__ img,
+                                                        uint64_t words) {
+  const uint64_t bytes = t.off[t.L];
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < words; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p0 = q * 8;
+    uint64_t w = 0;
+    bool done = false;
+    if (t.L > 0 && p0 >= t.off[0]) {
+      int l = find_layer(t.off, t.L, p0);
+      const uint64_t d = t.off[l] + 12;  // first value byte of layer l
+      if (p0 >= d && p0 + 8 <= t.off[l + 1]) {
+        const uint64_t rel = p0 - d, k = rel >> 3;
+        const int m = (int)(rel & 7);
+        w = value_bits(t, l, k) >> (8 * m);
+        if (m) w |= value_bits(t, l, k + 1) << (64 - 8 * m);
+        done = true;
+      }
+    }
+    if (!done) {
+      for (int b = 0; b < 8; ++b)
+        if (p0 + b < bytes) w |= (uint64_t)image_byte(t, p0 + b) << (8 * b);
+    }
+    img[q] = w;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_ckpt_unpack(const __grid_constant__ CkptTable t,
+                                                          const uint64_t* __restrict__ img) {
+  const uint64_t total = t.cum[t.L];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int l = find_layer(t.cum, t.L, i);  // the largest such l skips empty layers
+    const uint64_t k = i - t.cum[l];
+    const uint64_t pos = t.off[l] + 12 + 8 * k;
+    const int m = (int)(pos & 7);
+    uint64_t bits = img[pos >> 3] >> (8 * m);
+    if (m) bits |= img[(pos >> 3) + 1] << (64 - 8 * m);
+    const double v = __longlong_as_double((long long)bits);
+    if (t.esz == 8)
+      static_cast<double*>(const_cast<void*>(t.p[l]))[k] = v;
+    else
+      static_cast<float*>(const_cast<void*>(t.p[l]))[k] = __double2float_rn(v);
+  }
+}
+
+int build_table(CkptTable& t, const void* const* layers, const uint64_t* counts, int L, int esz) {
+  if (L < 0 || L > kMaxLayers) return fail(PGX_E_CONFIG, "checkpoint layer count %d outside 0..%d", L, kMaxLayers);
+  if (esz != 4 && esz != 8) return fail(PGX_E_CONFIG, "element size %d is not 4 or 8", esz);
+  t.L = L;
+  t.esz = esz;
+  t.off[0] = 5;
+  t.cum[0] = 0;
+  for (int l = 0; l < L; ++l) {
+    if (counts[l] && !layers[l]) return fail(PGX_E_INPUT, "layer %d has no data pointer", l);
+    t.p[l] = layers[l];
+    t.off[l + 1] = t.off[l] + 12 + 8 * counts[l];
+    t.cum[l + 1] = t.cum[l] + counts[l];
+  }
+  return PGX_OK;
+}
+
+int grid_for(uint64_t items) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t want = (items + kThreads - 1) / kThreads, cap = (uint64_t)sms * 8;
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+// Python's repr() of a bytes object (the reference formats the bad magic with !r).
+std::string py_bytes_repr(const uint8_t* b, size_t n) {
+  bool sq = false, dq = false;
+  for (size_t i = 0; i < n; ++i) {
+    sq |= b[i] == '\'';
+    dq |= b[i] == '"';
+  }
+  const char quote = (sq && !dq) ? '"' : '\'';
+  std::string s = "b";
+  s += quote;
+  char tmp[8];
+  for (size_t i = 0; i < n; ++i) {
+    uint8_t c = b[i];
+    if (c == (uint8_t)quote || c == '\\') {
+      s += '\\';
+      s += (char)c;
+    } else if (c == '\t') {
+      s += "\\t";
+    } else if (c == '\n') {
+      s += "\\n";
+    } else if (c == '\r') {
+      s += "\\r";
+    } else if (c < 0x20 || c >= 0x7f) {
+      snprintf(tmp, sizeof(tmp), "\\x%02x", c);
+      s += tmp;
+    } else {
+      s += (char)c;
+    }
+  }
+  s += quote;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pgx_ckpt_image_bytes(const uint64_t* counts, int num_layers, uint64_t* bytes_out) {
+  if (num_layers < 0) return fail(PGX_E_CONFIG, "negative layer count");
+  uint64_t b = 5;
+  for (int l = 0; l < num_layers; ++l) b += 12 + 8 * counts[l];
+  *bytes_out = b;
+  return PGX_OK;
+}
+
+int pgx_ckpt_parse(const void* blob, uint64_t bytes, uint64_t* counts_out, int capacity, int* num_layers_out) {
+  const uint8_t* b = static_cast<const uint8_t*>(blob);
+  static const uint8_t magic[5] = {'P', 'S', 'G', 'D', '1'};
+  if (bytes < 5 || memcmp(b, magic, 5) != 0)
+    return fail(PGX_E_FORMAT, "bad checkpoint magic %s", py_bytes_repr(b, bytes < 5 ? bytes : 5).c_str());
+  uint64_t pos = 5;
+  int n = 0;
+  while (pos < bytes) {
+    if (bytes - pos < 12) return fail(PGX_E_FORMAT, "truncated checkpoint: partial layer header");
+    uint32_t index;
+    uint64_t count;
+    memcpy(&index, b + pos, 4);  // little-endian host (x86-64 / aarch64)
+    memcpy(&count, b + pos + 4, 8);
+    pos += 12;
+    if (index != (uint32_t)n) return fail(PGX_E_FORMAT, "layer %d recorded with index %u", n, index);
+    if (count > (bytes - pos) / 8) return fail(PGX_E_FORMAT, "truncated checkpoint: layer %u shorter than declared", index);
+    if (counts_out && n < capacity) counts_out[n] = count;
+    ++n;
+    pos += count * 8;
+  }
+  if (n == 0) return fail(PGX_E_FORMAT, "checkpoint holds no layers");
+  *num_layers_out = n;
+  if (counts_out && n > capacity) return fail(PGX_E_RANGE, "checkpoint holds %d layers, capacity %d", n, capacity);
+  return PGX_OK;
+}
+
+int pgx_ckpt_pack(const void* const* layers, const uint64_t* counts, int num_layers, int elem_size, void* image,
+                  uint64_t capacity, void* stream) {
+  std::unique_ptr<CkptTable> tp(new CkptTable());  // 12 KB; the launch copies it
+  CkptTable& t = *tp;
+  int rc = build_table(t, layers, counts, num_layers, elem_size);
+  if (rc) return rc;
+  const uint64_t bytes = t.off[num_layers], words = (bytes + 7) / 8;
+  if (capacity < words * 8) return fail(PGX_E_RANGE, "image buffer %llu bytes < %llu", (unsigned long long)capacity,
+                                        (unsigned long long)(words * 8));
+  if (reinterpret_cast<uintptr_t>(image) & 7) return fail(PGX_E_INPUT, "image buffer is not 8-byte aligned");
+  k_ckpt_pack<<<grid_for(words), kThreads, 0, (cudaStream_t)stream>>>(t, static_cast<uint64_t*>(image), words);
+  PGX_LAUNCH_CHECK();
+  return PGX_OK;
+}
+
+int pgx_ckpt_unpack(const void* image, uint64_t capacity, const uint64_t* counts, int num_layers, int elem_size,
+                    void* const* layers, void* stream) {
+  std::unique_ptr<CkptTable> tp(new CkptTable());
+  CkptTable& t = *tp;
+  int rc = build_table(t, const_cast<const void* const*>(layers), counts, num_layers, elem_size);
+  if (rc) return rc;
+  const uint64_t need = (t.off[num_layers] + 7) / 8 * 8 + 8;  // the last value reads one word past its own
+  if (capacity < need) return fail(PGX_E_RANGE, "image buffer %llu bytes < %llu", (unsigned long long)capacity,
+                                   (unsigned long long)need);
+  if (reinterpret_cast<uintptr_t>(image) & 7) return fail(PGX_E_INPUT, "image buffer is not 8-byte aligned");
+  if (t.cum[num_layers] == 0) return PGX_OK;
+  k_ckpt_unpack<<<grid_for(t.cum[num_layers]), kThreads, 0, (cudaStream_t)stream>>>(
+      t, static_cast<const uint64_t*>(image));
+  PGX_LAUNCH_CHECK();
+  return PGX_OK;
+}
+
+}  // extern "C"

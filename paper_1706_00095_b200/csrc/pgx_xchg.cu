@@ -80,6 +80,7 @@ struct XArgs {
   uint32_t push_items, items;
   uint32_t item_begin, item_end;       // claimed range (phase selection)
   uint64_t olo, ohi;                   // TWOSHOT_CE owner sub-range (ohi == 0: the whole shard)
+  int single_buffer;                   // rx parity fixed at 0 (TWOSHOT_CEP: host-addressed copies)
   const uint32_t* iter;                // device iteration counter (graph mode) or null
   double lr;
   float scale, mu, wd;
@@ -338,7 +339,7 @@ template <int N, class T, bool kTma>
 __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot(XArgs a) {
   constexpr int W = VecT<T>::W;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
-  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  const int parity = a.single_buffer ? 0 : (a.iter ? (int)(*a.iter & 1) : a.parity);
   extern __shared__ __align__(128) uint8_t tma_buf[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(tma_buf + kTmaStages * kTmaStage);
   uint32_t tma_phase = 0;
@@ -802,6 +803,20 @@ __global__ void k_signal(FlagOut fo, uint32_t value, const uint32_t* iter) {
   }
 }
 
+// Raise every chunk flag of each peer's slot (after this stream's copies, stream order).
+struct FlagRanges {
+  uint32_t* f[PGX_MAX_RANKS];
+  uint32_t n[PGX_MAX_RANKS];
+  int k;
+};
+__global__ void k_signal_range(FlagRanges fr, uint32_t value, const uint32_t* iter) {
+  const uint32_t v = iter ? *iter + 1 : value;
+  if (threadIdx.x == 0) fence_acq_rel_sys();
+  __syncthreads();
+  for (int q = 0; q < fr.k; ++q)
+    for (uint32_t c = threadIdx.x; c < fr.n[q]; c += blockDim.x) st_release_sys(fr.f[q] + c, v);
+}
+
 __global__ void k_tick(uint32_t* iter) { *iter += 1; }
 
 // Whole-model gate: every (flag, multiplier) entry of every layer in one launch;
@@ -835,11 +850,14 @@ __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
     owner_vectors<N, T, U, false>(a, rxb, lo, hi, blk * span + threadIdx.x, nvec);
 }
 
+constexpr int kCepCtas = 48;  // TWOSHOT_CEP owner grid default
+
 struct LayerPlan {
   uint64_t S = 0;
   int variant = 0;
   uint64_t sl = 0;       // shard elems (twoshot) or S (tree)
   uint32_t C = 0;        // chunks per shard / per layer
+  uint64_t CH = 0;       // chunk elems (notification granularity) of this layer
   int K = 0;             // rx slots per parity
   uint64_t model_off = 0, rx_off = 0;
   uint64_t rxflag_off = 0;
@@ -952,7 +970,7 @@ XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
   a.v = x->v ? x->v + P.model_off : nullptr;
   a.S = P.S;
   a.sl = P.sl;
-  a.CH = x->cfg.chunk_elems;
+  a.CH = P.CH;
   a.C = P.C;
   a.K = P.K;
   a.dflag = P.dflag;
@@ -1229,7 +1247,7 @@ static int launch_nvls(pgx_xchg* x, int l, const LayerPlan& P, const XArgs& a, c
   n.queue = a.queue;
   n.S = P.S;
   n.sl = P.sl;
-  n.CH = x->cfg.chunk_elems;
+  n.CH = P.CH;
   n.pub_items = P.push_items;
   n.items = P.items;
   n.epoch = a.epoch;
@@ -1395,6 +1413,79 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
   return PGX_OK;
 }
 
+// TWOSHOT_CEP launch: the reduce-scatter as copy-engine peer copies (one per peer, the
+// sizes where the copy engines run at full rate), then one k_signal_range raising every
+// chunk flag of the shard; the owner side is the SM two-shot kernel's owner items
+// (tree-order fold + fused update + all-gather peer stores + arrival counters) on its
+// own stream behind a one-CTA wait, so its CTAs do not spin while the copies fly.
+static int launch_twoshot_cep(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, cudaStream_t s, int phases) {
+  const int N = x->world, me = x->rank, esz = x->esz;
+  a.single_buffer = 1;  // host-addressed copies: parity 0 (safe: senders gate on the previous all-gather)
+  a.parity = 0;
+  cudaError_t e = xrecord(x->ready[l], s);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "event: %s", cudaGetErrorString(e));
+  auto shard = [&](int j, uint64_t& lo, uint64_t& hi) {
+    lo = std::min(P.S, (uint64_t)j * P.sl);
+    hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
+  };
+  if (phases & PGX_PHASE_PUSH) {
+    xwait(x->ce_rs, x->ready[l]);
+    FlagRanges fr{};
+    for (int d = 1; d < N; ++d) {
+      int j = (me + d) % N;
+      uint64_t lo, hi;
+      shard(j, lo, hi);
+      if (lo >= hi) continue;
+      uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)me * P.sl) * esz;
+      uint64_t pb = 0;
+      for (int k = 0; k < a.g.n; ++k) {
+        uint64_t pe = a.g.end[k];
+        uint64_t ol = std::max(lo, pb), oh = std::min(hi, pe);
+        if (ol < oh) {
+          e = cudaMemcpyAsync(dst + (ol - lo) * esz, static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz,
+                              (oh - ol) * esz, cudaMemcpyDeviceToDevice, x->ce_rs);
+          if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
+        }
+        pb = pe;
+      }
+      fr.f[fr.k] = a.rxflags[j] + (uint64_t)me * P.C;
+      fr.n[fr.k++] = (uint32_t)((hi - lo + P.CH - 1) / P.CH);
+    }
+    if (fr.k) {
+      k_signal_range<<<1, 256, 0, x->ce_rs>>>(fr, a.epoch, a.iter);
+      ++x->launches;
+    }
+    xrecord(x->rs_done[l], x->ce_rs);
+  }
+  if (phases & PGX_PHASE_OWNER) {
+    xwait(x->ce_own, x->ready[l]);
+    uint64_t lo, hi;
+    shard(me, lo, hi);
+    const uint32_t mine = lo < hi ? (uint32_t)((hi - lo + P.CH - 1) / P.CH) : 0;
+    if (mine && N > 1) {  // every peer raises all of a shard's flags at once: wait on the last one
+      FlagSet fs{};
+      for (int sidx = 0; sidx < N; ++sidx)
+        if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C + (mine - 1);
+      k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
+      ++x->launches;
+    }
+    a.item_begin = P.push_items;
+    a.item_end = P.items;
+    if (mine) {
+      int grid = (int)std::min<uint32_t>(mine, (uint32_t)P.grid);
+      ++x->launches;
+      if (esz == 8)
+        launch_twoshot<double>(N, false, grid, x->dev, x->ce_own, a);
+      else
+        launch_twoshot<float>(N, false, grid, x->dev, x->ce_own, a);
+    }
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = xrecord(x->done[l], x->ce_own);
+    if (e != cudaSuccess) return fail(PGX_E_CUDA, "exchange launch failed: %s", cudaGetErrorString(e));
+  }
+  return PGX_OK;
+}
+
 extern "C" {
 
 int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
@@ -1412,11 +1503,10 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   x->seg_model = cfg->seg_base;
   x->seg_rx = cfg->seg_base + 1;
   const int N = x->world;
-  const uint64_t CH = cfg->chunk_elems;
   int kmax = 0;
   for (int r = 0; r < N; ++r) kmax = std::max(kmax, tree_num_children(r, N));
   int sms = sm_count(x->dev);
-  int cap = cfg->max_ctas > 0 ? cfg->max_ctas : 2 * sms;
+  const int cap_all = cfg->max_ctas > 0 ? cfg->max_ctas : 2 * sms;
   uint64_t moff = 0, rxoff = 0, rxfoff = 0;
   uint32_t dflag = cfg->num_layers;
   x->L.resize(cfg->num_layers);
@@ -1428,13 +1518,29 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       return fail(PGX_E_CONFIG, "layer %d has no elements", l);
     }
     P.variant = cfg->variant ? cfg->variant[l] : PGX_VARIANT_TWOSHOT;
+    const uint64_t CH = (cfg->layer_chunk_elems && cfg->layer_chunk_elems[l]) ? cfg->layer_chunk_elems[l]
+                                                                              : cfg->chunk_elems;
+    if (CH < 4 || CH % 4) {
+      delete x;
+      return fail(PGX_E_CONFIG, "layer %d: chunk_elems must be a positive multiple of 4", l);
+    }
+    P.CH = CH;
+    // per-layer CTA cap (large layers: fewer CTAs with bigger chunks leave SMs to the backward)
+    const bool lcapped = cfg->layer_max_ctas && cfg->layer_max_ctas[l] > 0;
+    int cap = lcapped ? cfg->layer_max_ctas[l] : cap_all;
+    bool capped = lcapped || cfg->max_ctas > 0;
+    if (P.variant == PGX_VARIANT_TWOSHOT_CEP && !capped) {  // 48 CTAs saturate NVLink (profiles/r3h)
+      cap = std::min(cap, kCepCtas);
+      capped = true;
+    }
     P.model_off = moff;
     moff = align_up(moff + P.S, kAlignElems);
     if (P.variant == PGX_VARIANT_NVLS && (cfg->mode != PGX_MODE_FAST32 || N < 2)) {
       delete x;
       return fail(PGX_E_CONFIG, "NVLS layers need fast32 and at least 2 ranks");
     }
-    if (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CE || P.variant == PGX_VARIANT_NVLS) {
+    if (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CE || P.variant == PGX_VARIANT_NVLS ||
+        P.variant == PGX_VARIANT_TWOSHOT_CEP) {
       P.sl = align_up((P.S + N - 1) / N, 4);
       P.C = (uint32_t)((P.sl + CH - 1) / CH);
       P.K = N;
@@ -1458,7 +1564,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
         P.items = P.push_items + P.C;
         P.expected = remote + my_chunks;  // every owner's chunks arrive by multicast, own ones included
       }
-      P.grid = (int)std::min<uint64_t>(P.items, cfg->max_ctas > 0 ? cap : (N == 1 ? 4 * sms : cap));
+      P.grid = (int)std::min<uint64_t>(P.items, capped ? cap : (N == 1 ? 4 * sms : cap));
       uint64_t own = my_hi - my_lo;
       P.nvlink_bytes = (N > 1) ? 2ull * (P.S - own) * x->esz : 0;  // RS out + AG out
       // owner fold: N partial reads + w (+v) read/write; pushes read the rest of the gradient
@@ -1683,6 +1789,11 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     xrecord(x->ready[l], s);
     int rc = launch_nvls(x, l, P, a, s);
     if (rc == PGX_OK) xrecord(x->done[l], s);
+    if (prev != x->dev) cudaSetDevice(prev);
+    return rc;
+  }
+  if (P.variant == PGX_VARIANT_TWOSHOT_CEP) {
+    int rc = launch_twoshot_cep(x, l, P, a, s, phases);
     if (prev != x->dev) cudaSetDevice(prev);
     return rc;
   }

@@ -24,17 +24,20 @@ from . import _lib
 from .errors import ConfigError, ShapeError
 
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
-            "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT}
+            "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32}
 
 
 def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20,
-                   oneshot_below: int | None = None) -> str:
+                   oneshot_below: int | None = None, large: str = "ce") -> str:
     """Layer-size policy (measured, profiles/r1*_sweep*): the smallest layers are pure
     latency and take the one-shot exchange (one NVLink hop); mid-size layers the SM
     two-shot kernel; layers of `ce_from` elements or more move their shards with the copy
     engines, which do not take SMs away from the backward kernels they overlap with.
-    `tree_below` optionally keeps the paper's tree for the smallest layers."""
+    `tree_below` optionally keeps the paper's tree for the smallest layers.  large="sm"
+    keeps the SM two-shot for the large layers too (run with a CTA cap and big chunks,
+    see DeviceExchange `large_ctas`); large="cep" moves the reduce-scatter by copy engine
+    and runs fold + update + all-gather as the SM owner kernel on a capped grid."""
     if oneshot_below is None:  # one-shot moves (N-1)*S per GPU: the crossover shrinks with N
         oneshot_below = (1 << 20) // max(world, 1)  # N=4: 1 MB layers (profiles/r2b_sweep_n4)
     if world > 1 and elems < tree_below:
@@ -42,7 +45,7 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
     if world > 1 and elems < oneshot_below:
         return "oneshot"
     if world > 1 and elems >= ce_from:
-        return "twoshot_ce"
+        return {"ce": "twoshot_ce", "cep": "twoshot_cep", "sm": "twoshot"}[large]
     return "twoshot"
 
 
@@ -50,7 +53,15 @@ class DeviceExchange:
     def __init__(self, transport, layer_elems, *, mode: str = "fast32", variant="twoshot",
                  chunk_elems: int = 16384, lr: float = 0.01, scale: float | None = None,
                  momentum: float = 0.0, weight_decay: float = 0.0, seg_base: int = 16, max_ctas: int = 0,
-                 tree_below: int = 0, low_priority_from: int | None = None):
+                 tree_below: int = 0, low_priority_from: int | None = None, large: str = "ce",
+                 large_from: int = 1 << 20, large_ctas: int = 0, large_chunk_elems: int = 0,
+                 layer_chunk_elems=None, layer_max_ctas=None):
+        """variant: one name, a per-layer list, or "auto" (choose_variant; `large` = "ce" or
+        "sm" for layers of >= `large_from` elements).  Layers of >= `large_from` elements get
+        `large_chunk_elems` / `large_ctas` (0 = the global chunk_elems / max_ctas): fewer CTAs
+        with bigger chunks move the same bytes with far fewer per-chunk system fences
+        (profiles/r3e), leaving SMs to the backward kernels.  layer_chunk_elems /
+        layer_max_ctas override per layer (0 = default)."""
         if mode not in MODES:
             raise ConfigError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
         self.tr = transport
@@ -60,7 +71,8 @@ class DeviceExchange:
         self.layer_elems = [int(n) for n in layer_elems]
         L = len(self.layer_elems)
         if isinstance(variant, str) and variant == "auto":
-            variants = [choose_variant(n, self.world, tree_below) for n in self.layer_elems]
+            variants = [choose_variant(n, self.world, tree_below, ce_from=large_from, large=large)
+                        for n in self.layer_elems]
         elif isinstance(variant, str):
             variants = [variant] * L
         else:
@@ -71,10 +83,21 @@ class DeviceExchange:
         self.scale = 1.0 / self.world if scale is None else float(scale)
         self._elems = (C.c_uint64 * L)(*self.layer_elems)
         self._vars = (C.c_int * L)(*[VARIANTS[v] for v in variants])
+        big = [n >= large_from for n in self.layer_elems]
+        chunks = list(layer_chunk_elems) if layer_chunk_elems is not None else \
+            [int(large_chunk_elems) if b else 0 for b in big]
+        ctas = list(layer_max_ctas) if layer_max_ctas is not None else [int(large_ctas) if b else 0 for b in big]
+        if len(chunks) != L or len(ctas) != L:
+            raise ConfigError("layer_chunk_elems / layer_max_ctas need one entry per layer")
+        self.layer_chunk_elems = [int(c) or int(chunk_elems) for c in chunks]
+        self.layer_max_ctas = [int(c) or int(max_ctas) for c in ctas]
+        self._chunks = (C.c_uint64 * L)(*[int(c) for c in chunks])
+        self._ctas = (C.c_int * L)(*[int(c) for c in ctas])
         cfg = _lib.XchgConfig(
             num_layers=L, layer_elems=self._elems, variant=self._vars, mode=MODES[mode],
             chunk_elems=int(chunk_elems), lr=float(lr), scale=self.scale, momentum=float(momentum),
-            weight_decay=float(weight_decay), seg_base=int(seg_base), max_ctas=int(max_ctas))
+            weight_decay=float(weight_decay), seg_base=int(seg_base), max_ctas=int(max_ctas),
+            layer_chunk_elems=self._chunks, layer_max_ctas=self._ctas)
         h = C.c_void_p()
         _lib.call("pgx_xchg_create", transport.handle, C.byref(cfg), C.byref(h))
         self.handle = h

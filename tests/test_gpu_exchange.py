@@ -35,7 +35,7 @@ def stepped_layer(xs, trs, l, k, pieces_by_rank):
 
     N = len(xs)
     sync = torch.cuda.synchronize
-    if xs[0].variants[l] in ("twoshot", "twoshot_ce", "oneshot"):
+    if xs[0].variants[l] in ("twoshot", "twoshot_ce", "twoshot_cep", "oneshot"):
         for r in range(N):
             xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
         sync()
@@ -63,7 +63,7 @@ def split_pieces(g, cut):
 
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "oneshot"])
+@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot"])
 @pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64"])
 def test_exchange_matches_oracle(cuda, N, variant, mode):
     elems = LENET if N in (2, 8) else CIFAR
@@ -171,7 +171,7 @@ class _FixedGrad(torch.nn.Module):
         return (self.weight * self.c).sum() + (self.bias * self.d).sum()
 
 
-@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce"])
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep"])
 @pytest.mark.parametrize("gate", ["layer", "model"])
 def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     """A captured training step (device iteration counter) applies exactly the oracle update."""
@@ -219,7 +219,7 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     world.close()
 
 
-@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "oneshot"])
+@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot"])
 def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
     """Layers smaller than one vector per rank (empty owner shards), ragged tails and a
     piece boundary inside a vector, 8 ranks stepped on one GPU, ref32 bit-exact."""
