@@ -159,8 +159,8 @@ int pgx_ckpt_image_bytes(const uint64_t* counts, int num_layers, uint64_t* bytes
 /* Host: walk and validate a PSGD1 blob (load_model_bytes, checkpoint.py:42-63);
  * counts_out may be NULL (count only).  PGX_E_FORMAT with the reference messages. */
 int pgx_ckpt_parse(const void* blob, uint64_t bytes, uint64_t* counts_out, int capacity, int* num_layers_out);
-/* Device: layers (elem_size 4 or 8) -> image (8-byte aligned, capacity >= bytes
- * rounded up to 8; the pad bytes are zero). */
+/* Device: layers (elem_size 4 or 8) -> image (16-byte aligned, capacity >= bytes
+ * rounded up to 16; the pad bytes are zero). */
 int pgx_ckpt_pack(const void* const* layers, const uint64_t* counts, int num_layers, int elem_size, void* image,
                   uint64_t capacity, void* stream);
 /* Device: image (8-byte aligned, capacity >= bytes rounded up to 8, plus 8) -> layers. */

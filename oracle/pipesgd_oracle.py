@@ -231,3 +231,83 @@ def exchange_iteration(grads, weights, eps: float, mode: str = "ref32", state=No
         v = state if state is not None else np.zeros_like(weights, dtype=np.float32)
         return fast32_update(weights, v, red, scale, eps if lr is None else lr, momentum, weight_decay)
     raise ValueError(mode)
+
+
+# ----------------------------------------------------------------------------- formats
+CKPT_MAGIC = b"PSGD1"  # engine/checkpoint.py:23
+
+
+class CheckpointFormatError(ValueError):
+    """Oracle-side stand-in for the reference's FormatError (errors.py:49)."""
+
+
+def ckpt_serialize(layers) -> bytes:
+    """PSGD1 image (engine/checkpoint.py:29-39): magic, then per layer little-endian
+    u32 index, u64 count and the values as '<f8' (fp32 promoted exactly)."""
+    parts = [CKPT_MAGIC]
+    for l, values in enumerate(layers):
+        a = np.ascontiguousarray(values, dtype="<f8")
+        if a.ndim != 1:
+            raise CheckpointFormatError(f"layer {l} is not a flat vector")
+        parts.append(np.array([l], "<u4").tobytes() + np.array([a.size], "<u8").tobytes())
+        parts.append(a.tobytes())
+    return b"".join(parts)
+
+
+def ckpt_load(blob: bytes) -> list:
+    """Walk and validate a PSGD1 image (engine/checkpoint.py:42-63), same checks and
+    messages in the same order; returns the f64 layers."""
+    if blob[:5] != CKPT_MAGIC:
+        raise CheckpointFormatError(f"bad checkpoint magic {blob[:5]!r}")
+    pos, out = 5, []
+    while pos < len(blob):
+        if len(blob) - pos < 12:
+            raise CheckpointFormatError("truncated checkpoint: partial layer header")
+        index = int(np.frombuffer(blob, "<u4", 1, pos)[0])
+        count = int(np.frombuffer(blob, "<u8", 1, pos + 4)[0])
+        pos += 12
+        if index != len(out):
+            raise CheckpointFormatError(f"layer {len(out)} recorded with index {index}")
+        if pos + 8 * count > len(blob):
+            raise CheckpointFormatError(f"truncated checkpoint: layer {index} shorter than declared")
+        out.append(np.frombuffer(blob, "<f8", count, pos).astype(np.float64))
+        pos += 8 * count
+    if not out:
+        raise CheckpointFormatError("checkpoint holds no layers")
+    return out
+
+
+def overlap_metrics(events):
+    """Run metrics of a timeline (timeline.py:137-175). events: (rank, iteration, layer,
+    kind, t0, t1).  Per rank: sum over COMM events of |event ∩ union(COMPUTE)| over the sum
+    of COMM lengths; averaged over ranks that communicated; wall clock per rank; run
+    iterations/s = (max iteration + 1) / span."""
+    comm_k = {"send_trigger", "recv_notify", "model_forward"}
+    comp_k = {"forward", "backward_layer", "reduce_local", "master_update"}
+    ranks = sorted({e[0] for e in events})
+    ratios, wall, per = [], {}, {}
+    for r in ranks:
+        ev = [e for e in events if e[0] == r]
+        spans = sorted((e[4], e[5]) for e in ev if e[3] in comp_k)
+        union = []
+        for a, b in spans:
+            if union and a <= union[-1][1]:
+                union[-1][1] = max(union[-1][1], b)
+            else:
+                union.append([a, b])
+        tot = hid = 0
+        for e in ev:
+            if e[3] in comm_k:
+                tot += e[5] - e[4]
+                hid += sum(max(0, min(e[5], hi) - max(e[4], lo)) for lo, hi in union)
+        wall[r] = max(e[5] for e in ev) - min(e[4] for e in ev)
+        if tot > 0:
+            per[r] = hid / tot
+            ratios.append(hid / tot)
+    ips = 0.0
+    if events:
+        span = max(e[5] for e in events) - min(e[4] for e in events)
+        if span > 0:
+            ips = (max(e[1] for e in events) + 1) / (span * 1e-9)
+    return {"overlap_ratio": sum(ratios) / len(ratios) if ratios else 0.0, "iterations_per_second": ips,
+            "wall_clock_ns": wall, "per_rank_overlap": per}

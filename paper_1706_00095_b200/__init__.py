@@ -25,7 +25,10 @@ _LAZY = {
     "DeviceExchange": "exchange", "ModuleBinding": "exchange",
     "run_local": "harness", "run_dist": "harness", "sequential_sgd": "harness",
     "verify_against_reference": "harness", "build_dataset": "harness",
-    "Recorder": "timeline", "compute_overlap": "timeline", "TimelineEvent": "timeline",
+    "Recorder": "timeline", "compute_overlap": "timeline", "TimelineEvent": "timeline", "RunMetrics": "timeline",
+    "read_timeline_csv": "timeline", "write_timeline_csv": "timeline",
+    "serialize_model": "checkpoint", "load_model_bytes": "checkpoint", "save_model": "checkpoint",
+    "load_model": "checkpoint", "Model": "checkpoint", "save_exchange": "checkpoint", "load_exchange": "checkpoint",
 }
 
 

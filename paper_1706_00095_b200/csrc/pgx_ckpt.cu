@@ -2,10 +2,10 @@
 //
 // Image (little-endian): "PSGD1", then per layer l: u32 l, u64 count, count x f64.
 // Layer l's header starts at off[l] = 5 + sum_{i<l} (12 + 8 n_i), so every value
-// sits at an odd byte offset: the pack kernel assembles each ALIGNED 8-byte output
-// word from the two values it straddles (one funnel shift) and writes it with one
-// 64-bit store, so a launch is a single coalesced HBM stream (read n*esz, write
-// 8n bytes); only words touching a header or the magic are built byte by byte.
+// sits at an odd byte offset: the pack kernel assembles each ALIGNED 16-byte output
+// pair from the three values it straddles (funnel shifts) and writes it with one
+// 128-bit store, so a launch is a single coalesced HBM stream (read n*esz, write
+// 8n bytes); only pairs touching a header or the magic are built byte by byte.
 // Unpack is the mirror: each value is read from its two aligned image words.
 // fp32 layers are promoted exactly to f64 on the way out (the reference
 // serializes np.asarray(values, "<f8")) and rounded to nearest on the way in.
@@ -63,29 +63,39 @@ __device__ uint8_t image_byte(const CkptTable& t, uint64_t pos) {
   return (uint8_t)(value_bits(t, l, r >> 3) >> (8 * (r & 7)));
 }
 
-__global__ void __launch_bounds__(kThreads) k_ckpt_pack(const __grid_constant__ CkptTable t, uint64_t* __restrict__ img,
-                                                        uint64_t words) {
+// One thread = one aligned 16-byte output pair (one 128-bit store).
+__global__ void __launch_bounds__(kThreads) k_ckpt_pack(const __grid_constant__ CkptTable t, uint4* __restrict__ img,
+                                                        uint64_t pairs) {
   const uint64_t bytes = t.off[t.L];
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < words; q += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t p0 = q * 8;
-    uint64_t w = 0;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < pairs; q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p0 = q * 16;
+    uint64_t w0 = 0, w1 = 0;
     bool done = false;
     if (t.L > 0 && p0 >= t.off[0]) {
-      int l = find_layer(t.off, t.L, p0);
+      const int l = find_layer(t.off, t.L, p0);
       const uint64_t d = t.off[l] + 12;  // first value byte of layer l
-      if (p0 >= d && p0 + 8 <= t.off[l + 1]) {
+      if (p0 >= d && p0 + 16 <= t.off[l + 1]) {
         const uint64_t rel = p0 - d, k = rel >> 3;
-        const int m = (int)(rel & 7);
-        w = value_bits(t, l, k) >> (8 * m);
-        if (m) w |= value_bits(t, l, k + 1) << (64 - 8 * m);
+        const int m = (int)(rel & 7);  // the same for every word of the layer
+        const uint64_t a = value_bits(t, l, k), b = value_bits(t, l, k + 1);
+        if (m) {
+          const uint64_t c = value_bits(t, l, k + 2);
+          w0 = (a >> (8 * m)) | (b << (64 - 8 * m));
+          w1 = (b >> (8 * m)) | (c << (64 - 8 * m));
+        } else {
+          w0 = a;
+          w1 = b;
+        }
         done = true;
       }
     }
-    if (!done) {
-      for (int b = 0; b < 8; ++b)
-        if (p0 + b < bytes) w |= (uint64_t)image_byte(t, p0 + b) << (8 * b);
+    if (!done) {  // touches the magic, a header, a layer edge or the padding
+      for (int b = 0; b < 8; ++b) {
+        if (p0 + b < bytes) w0 |= (uint64_t)image_byte(t, p0 + b) << (8 * b);
+        if (p0 + 8 + b < bytes) w1 |= (uint64_t)image_byte(t, p0 + 8 + b) << (8 * b);
+      }
     }
-    img[q] = w;
+    img[q] = make_uint4((uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32));
   }
 }
 
@@ -208,11 +218,11 @@ int pgx_ckpt_pack(const void* const* layers, const uint64_t* counts, int num_lay
   CkptTable& t = *tp;
   int rc = build_table(t, layers, counts, num_layers, elem_size);
   if (rc) return rc;
-  const uint64_t bytes = t.off[num_layers], words = (bytes + 7) / 8;
-  if (capacity < words * 8) return fail(PGX_E_RANGE, "image buffer %llu bytes < %llu", (unsigned long long)capacity,
-                                        (unsigned long long)(words * 8));
-  if (reinterpret_cast<uintptr_t>(image) & 7) return fail(PGX_E_INPUT, "image buffer is not 8-byte aligned");
-  k_ckpt_pack<<<grid_for(words), kThreads, 0, (cudaStream_t)stream>>>(t, static_cast<uint64_t*>(image), words);
+  const uint64_t bytes = t.off[num_layers], pairs = (bytes + 15) / 16;
+  if (capacity < pairs * 16) return fail(PGX_E_RANGE, "image buffer %llu bytes < %llu", (unsigned long long)capacity,
+                                         (unsigned long long)(pairs * 16));
+  if (reinterpret_cast<uintptr_t>(image) & 15) return fail(PGX_E_INPUT, "image buffer is not 16-byte aligned");
+  k_ckpt_pack<<<grid_for(pairs), kThreads, 0, (cudaStream_t)stream>>>(t, static_cast<uint4*>(image), pairs);
   PGX_LAUNCH_CHECK();
   return PGX_OK;
 }
