@@ -383,12 +383,43 @@ def pgx_arm(args):
     # ---- end-to-end through the public API: host batch in, loss out ----
     e2e = None
     if not args.no_e2e:
+        # every step's batch crosses from pinned host memory inside the timed region, as a
+        # data loader would deliver it: step i+1's H2D copy (copy engine, own stream) is
+        # issued before step i's compute so it overlaps it; a 13 us D2D copy installs it
+        # into the graph's static input once step i has finished reading the previous one
+        h2d = torch.cuda.Stream(device=dev)
+        stage = [(torch.empty_like(dev_x), torch.empty_like(dev_y)) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        consumed = [None, None]
+
+        def prefetch(j):
+            b = j % 2
+            with torch.cuda.stream(h2d):
+                if consumed[b] is not None:
+                    h2d.wait_event(consumed[b])
+                stage[b][0].copy_(host_x, non_blocking=True)
+                stage[b][1].copy_(host_y, non_blocking=True)
+                ready[b].record(h2d)
+
         def e2e_step(i):
-            loss = run_step(host_x, host_y)
+            b = i % 2
+            cur = torch.cuda.current_stream(dev)
+            if i == 0:
+                prefetch(0)
+            cur.wait_event(ready[b])
+            dev_x.copy_(stage[b][0], non_blocking=True)
+            dev_y.copy_(stage[b][1], non_blocking=True)
+            consumed[b] = torch.cuda.Event()
+            consumed[b].record(cur)
+            if i + 1 < args.steps:
+                prefetch(i + 1)
+            loss = run_step()
             loss_host[i % loss_host.numel()].copy_(loss.detach(), non_blocking=True)
         ms_e2e = timed(e2e_step, args.steps)
         h2d = (host_x.numel() * host_x.element_size() + host_y.numel() * host_y.element_size()) * world
         e2e = {"value": gb * args.steps / (ms_e2e / 1e3), "unit": "images/s",
+               "input_pipeline": "pinned host batch -> device by copy engine on a side stream, one step "
+                                 "ahead (double-buffered), inside the timed region; loss read back every step",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * world, "ms_per_step": ms_e2e / args.steps,
                "final_loss": float(loss_host[(args.steps - 1) % loss_host.numel()])}
 
