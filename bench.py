@@ -475,7 +475,8 @@ def pgx_arm(args):
                 continue
             ms_l = iso[0] if l == L_DOM else isolated(l)
             busbw = 2 * (world - 1) / world * n * 4 / (ms_l / 1e3) / 1e9
-            by_layer.append({"layer": l, "bytes": n * 4, "variant": xchg.variants[l], "isolated_ms": ms_l,
+            by_layer.append({"layer": l, "bytes": n * 4, "variant": xchg.variants[l], "chunk_elems": xchg.layer_plan(l)[0],
+                             "isolated_ms": ms_l,
                              "busbw_gbs": busbw, "frac_of_770": busbw / NVLINK_PEAK_GBS})
 
     # the same large layers through the SM two-shot kernel (not the in-step choice at N>1 when
@@ -483,7 +484,7 @@ def pgx_arm(args):
     by_layer_sm = []
     if world > 1 and by_layer and any(r["variant"] != "twoshot" for r in by_layer):
         alt = DeviceExchange(tr, sizes, mode="fast32", variant="twoshot", chunk_elems=args.chunk_elems,
-                             scale=1.0 / world, seg_base=24, large_chunk_elems=65536, **wl["hyper"])
+                             scale=1.0 / world, seg_base=24, **wl["hyper"])
         tr.sync_segments()
         alt.connect()
         for r in by_layer:
@@ -505,7 +506,7 @@ def pgx_arm(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_l = float(t.item())
             busbw = 2 * (world - 1) / world * n * 4 / (ms_l / 1e3) / 1e9
-            by_layer_sm.append({"layer": l, "bytes": n * 4, "variant": "twoshot", "chunk_elems": alt.layer_chunk_elems[l],
+            by_layer_sm.append({"layer": l, "bytes": n * 4, "variant": "twoshot", "chunk_elems": alt.layer_plan(l)[0],
                                 "isolated_ms": ms_l,
                                 "busbw_gbs": busbw, "frac_of_770": busbw / NVLINK_PEAK_GBS})
         tr.barrier()

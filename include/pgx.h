@@ -137,7 +137,9 @@ int pgx_tree_reduce_f32(const float* const* partials, int world, float* out, uin
 enum pgx_mode {
   PGX_MODE_REF64 = 0,  /* f64 storage, bit-exact with the reference engine      */
   PGX_MODE_REF32 = 1,  /* f32 storage, reference ops applied to fp32 arrays      */
-  PGX_MODE_FAST32 = 2  /* f32: g*scale + wd*w, v = mu*v + lr*g, w -= v           */
+  PGX_MODE_FAST32 = 2, /* f32: g*scale + wd*w, v = mu*v + lr*g, w -= v           */
+  PGX_MODE_SUM32 = 3   /* f32, update off: w = scale * (tree-order sum) — an all-reduce
+                          (average) with the same fold order; the sweep's NCCL peer */
 };
 /* Master-side fused _advance_folds + _apply_update (pipelined.py:103-108,
  * 158-188): tree-order fold of `world` partials, then the update in place on
@@ -203,7 +205,9 @@ typedef struct pgx_xchg_config {
   const uint64_t* layer_elems;   /* S_l, elements per layer ([W row-major][b]) */
   const int* variant;            /* per layer pgx_variant */
   int mode;                      /* pgx_mode (REF64 uses double elements) */
-  uint64_t chunk_elems;          /* notification granularity, multiple of 4 */
+  uint64_t chunk_elems;          /* notification granularity, multiple of 4; with N > 1
+                                    the two-shot variants double it up to 65536 while a
+                                    shard still has >= 128 chunks (fewer system fences) */
   double lr;                     /* epsilon / learning rate */
   float scale, momentum, weight_decay;
   uint32_t seg_base;             /* segment ids seg_base (weights + arrival flags) and
@@ -273,6 +277,9 @@ int pgx_xchg_gate_all(pgx_xchg* x, uint32_t iteration, void* stream);
 /* Per-layer launch statistics for the roofline (bytes moved per launch). */
 int pgx_xchg_layer_bytes(pgx_xchg* x, int layer, uint64_t* nvlink_out_bytes,
                          uint64_t* hbm_bytes);
+/* The plan a layer runs with: effective chunk elements (notification granularity) and
+ * CTAs of its exchange kernel launch. */
+int pgx_xchg_layer_plan(pgx_xchg* x, int layer, uint64_t* chunk_elems_out, int* ctas_out);
 
 #ifdef __cplusplus
 }

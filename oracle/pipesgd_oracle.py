@@ -230,6 +230,9 @@ def exchange_iteration(grads, weights, eps: float, mode: str = "ref32", state=No
         red = tree_reduce([[g] for g in grads], world, np.float32)[0]
         v = state if state is not None else np.zeros_like(weights, dtype=np.float32)
         return fast32_update(weights, v, red, scale, eps if lr is None else lr, momentum, weight_decay)
+    if mode == "sum32":  # update off: the averaged all-reduce result, fl(scale * tree_sum) (no reference counterpart)
+        red = tree_reduce([[g] for g in grads], world, np.float32)[0]
+        return (np.float32(scale) * red).astype(np.float32)
     raise ValueError(mode)
 
 

@@ -24,7 +24,7 @@ MAX_PIECES = 4
 XCHG_STREAMS = 5
 CKPT_MAX_LAYERS = 512
 
-MODE_REF64, MODE_REF32, MODE_FAST32 = 0, 1, 2
+MODE_REF64, MODE_REF32, MODE_FAST32, MODE_SUM32 = 0, 1, 2, 3
 VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE, VARIANT_NVLS, VARIANT_ONESHOT = 0, 1, 2, 3, 4
 VARIANT_TWOSHOT_CEP = 5
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
@@ -100,6 +100,7 @@ SIGNATURES = {
     "pgx_xchg_nvls_import": [vp, i32],
     "pgx_xchg_nvls_bind": [vp],
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
+    "pgx_xchg_layer_plan": [vp, i32, P(u64), P(i32)],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],
     "pgx_xchg_set_streams": [vp, P(vp), i32],

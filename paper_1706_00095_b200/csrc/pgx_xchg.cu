@@ -146,6 +146,7 @@ __device__ __forceinline__ T apply_update(T w, T g, float& v, const XArgs& a) {
     return __dsub_rn(w, __dmul_rn(a.lr, g));
   } else {
     if (a.mode == PGX_MODE_REF32) return __double2float_rn(__dsub_rn((double)w, __dmul_rn(a.lr, (double)g)));
+    if (a.mode == PGX_MODE_SUM32) return __fmul_rn(a.scale, g);
     float gg = __fadd_rn(__fmul_rn(a.scale, g), __fmul_rn(a.wd, w));
     float vv = __fadd_rn(__fmul_rn(a.mu, v), __fmul_rn((float)a.lr, gg));
     v = vv;
@@ -198,7 +199,12 @@ __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint
         else
           ld_vec<T>(rxb + (uint64_t)s * a.sl + q * W, cnt[u], vals[u][s]);
       }
-      ld_vec<T>(static_cast<const T*>(a.model[me]) + e, cnt[u], w[u]);
+      if (a.mode != PGX_MODE_SUM32) {  // update off: the weights are not an input
+        ld_vec<T>(static_cast<const T*>(a.model[me]) + e, cnt[u], w[u]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < W; ++k) w[u][k] = T(0);
+      }
       if (fast) ld_vec<float>(a.v + e, cnt[u], vv[u]);
     }
   }
@@ -851,6 +857,7 @@ __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
 }
 
 constexpr int kCepCtas = 48;  // TWOSHOT_CEP owner grid default
+constexpr uint64_t kAutoChunkMax = 65536;  // elements
 
 struct LayerPlan {
   uint64_t S = 0;
@@ -1491,7 +1498,7 @@ extern "C" {
 int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   if (!cfg || cfg->num_layers < 1) return fail(PGX_E_CONFIG, "exchange needs at least one layer");
   if (cfg->chunk_elems < 4 || cfg->chunk_elems % 4) return fail(PGX_E_CONFIG, "chunk_elems must be a positive multiple of 4");
-  if (cfg->mode < 0 || cfg->mode > 2) return fail(PGX_E_CONFIG, "unknown mode %d", cfg->mode);
+  if (cfg->mode < 0 || cfg->mode > 3) return fail(PGX_E_CONFIG, "unknown mode %d", cfg->mode);
   if (!(cfg->lr > 0)) return fail(PGX_E_CONFIG, "epsilon must be > 0, got %g", cfg->lr);
   pgx_xchg* x = new pgx_xchg();
   x->w = w;
@@ -1518,8 +1525,16 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       return fail(PGX_E_CONFIG, "layer %d has no elements", l);
     }
     P.variant = cfg->variant ? cfg->variant[l] : PGX_VARIANT_TWOSHOT;
-    const uint64_t CH = (cfg->layer_chunk_elems && cfg->layer_chunk_elems[l]) ? cfg->layer_chunk_elems[l]
-                                                                              : cfg->chunk_elems;
+    const bool ch_given = cfg->layer_chunk_elems && cfg->layer_chunk_elems[l];
+    uint64_t CH = ch_given ? cfg->layer_chunk_elems[l] : cfg->chunk_elems;
+    if (!ch_given && N > 1 && (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CEP)) {
+      // big shards: chunks of up to 64 K elements (~128 per shard) amortise the system fence
+      // that ends every chunk; chunk_elems stays the minimum (profiles/r3e, r3n)
+      const uint64_t target = (P.S + N - 1) / N / 128;
+      uint64_t c = CH;
+      while (c * 2 <= target && c * 2 <= kAutoChunkMax) c *= 2;
+      CH = c;
+    }
     if (CH < 4 || CH % 4) {
       delete x;
       return fail(PGX_E_CONFIG, "layer %d: chunk_elems must be a positive multiple of 4", l);
@@ -1568,7 +1583,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       uint64_t own = my_hi - my_lo;
       P.nvlink_bytes = (N > 1) ? 2ull * (P.S - own) * x->esz : 0;  // RS out + AG out
       // owner fold: N partial reads + w (+v) read/write; pushes read the rest of the gradient
-      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0)) * own * x->esz +
+      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0)) * own * x->esz +
                     (P.S - own) * x->esz;
 
     } else if (P.variant == PGX_VARIANT_ONESHOT) {
@@ -1584,7 +1599,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       P.expected = 0;  // each rank updates its own copy
       P.grid = (int)std::min<uint64_t>(P.items, cap);
       P.nvlink_bytes = (uint64_t)(N - 1) * P.S * x->esz;
-      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0)) * P.S * x->esz +
+      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0)) * P.S * x->esz +
                     (uint64_t)(N - 1) * P.S * x->esz;
     } else if (P.variant == PGX_VARIANT_TREE) {
       P.sl = align_up(P.S, kAlignElems);  // slot stride keeps every slot 16B-aligned
@@ -1605,7 +1620,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       P.down_grid = (int)std::min<uint64_t>(P.down_items, cap);
       uint64_t out_up = x->rank ? P.S : 0;
       P.nvlink_bytes = (out_up + (uint64_t)nc * P.S) * x->esz;
-      P.hbm_bytes = ((uint64_t)nc + 1 + (x->rank == 0 ? 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : 0) : 0)) * P.S * x->esz;
+      P.hbm_bytes = ((uint64_t)nc + 1 + (x->rank == 0 ? 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0) : 0)) * P.S * x->esz;
     } else {
       delete x;
       return fail(PGX_E_CONFIG, "layer %d: unknown variant %d", l, P.variant);
@@ -1985,6 +2000,13 @@ int pgx_xchg_layer_bytes(pgx_xchg* x, int l, uint64_t* nvl, uint64_t* hbm) {
   if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
   if (nvl) *nvl = x->L[l].nvlink_bytes;
   if (hbm) *hbm = x->L[l].hbm_bytes;
+  return PGX_OK;
+}
+
+int pgx_xchg_layer_plan(pgx_xchg* x, int l, uint64_t* chunk_elems, int* ctas) {
+  if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
+  if (chunk_elems) *chunk_elems = x->L[l].CH;
+  if (ctas) *ctas = x->L[l].grid;
   return PGX_OK;
 }
 

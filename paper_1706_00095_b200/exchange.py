@@ -25,7 +25,7 @@ from .errors import ConfigError, ShapeError
 
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
             "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP}
-MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32}
+MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 
 def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20,
@@ -89,7 +89,7 @@ class DeviceExchange:
         ctas = list(layer_max_ctas) if layer_max_ctas is not None else [int(large_ctas) if b else 0 for b in big]
         if len(chunks) != L or len(ctas) != L:
             raise ConfigError("layer_chunk_elems / layer_max_ctas need one entry per layer")
-        self.layer_chunk_elems = [int(c) or int(chunk_elems) for c in chunks]
+        self._chunks_req = [int(c) for c in chunks]
         self.layer_max_ctas = [int(c) or int(max_ctas) for c in ctas]
         self._chunks = (C.c_uint64 * L)(*[int(c) for c in chunks])
         self._ctas = (C.c_int * L)(*[int(c) for c in ctas])
@@ -185,6 +185,12 @@ class DeviceExchange:
         nvl, hbm = C.c_uint64(), C.c_uint64()
         _lib.call("pgx_xchg_layer_bytes", self.handle, layer, C.byref(nvl), C.byref(hbm))
         return nvl.value, hbm.value
+
+    def layer_plan(self, layer: int) -> tuple[int, int]:
+        """(effective chunk elements, CTAs of the layer's kernel launch)."""
+        ch, ctas = C.c_uint64(), C.c_int()
+        _lib.call("pgx_xchg_layer_plan", self.handle, layer, C.byref(ch), C.byref(ctas))
+        return ch.value, ctas.value
 
     # -- per-layer operations ------------------------------------------------------
     def stream_for(self, layer: int):

@@ -64,7 +64,7 @@ def split_pieces(g, cut):
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot"])
-@pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64"])
+@pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64", "sum32"])
 def test_exchange_matches_oracle(cuda, N, variant, mode):
     elems = LENET if N in (2, 8) else CIFAR
     iters = 3
@@ -88,6 +88,8 @@ def test_exchange_matches_oracle(cuda, N, variant, mode):
             if mode == "fast32":
                 w[l], v[l] = O.exchange_iteration(grads, w[l], 0.01, mode, state=v[l], scale=1.0 / N,
                                                   momentum=0.9, weight_decay=5e-4)
+            elif mode == "sum32":  # update off: every rank holds the averaged tree-order sum
+                w[l] = O.exchange_iteration(grads, w[l], 0.05, mode, scale=1.0 / N)
             else:
                 w[l] = O.exchange_iteration(grads, w[l], 0.05, mode).astype(dt)
             for r in range(N):

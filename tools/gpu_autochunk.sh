@@ -1,0 +1,8 @@
+#!/bin/bash
+n=$(python -c "import torch;print(torch.cuda.device_count())")
+t=r3o
+timeout 1500 python -m pytest tests/test_gpu_exchange.py tests/test_gpu_multi.py -q -x -p no:cacheprovider -rf > gpurun_out/${t}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${t}_pytest.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29581 tools/sweep.py --variants twoshot,tree,twoshot_ce,twoshot_cep,oneshot,nccl --mode fast32 > gpurun_out/${t}_sweep_fast32.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29582 tools/sweep.py --variants twoshot,nccl --mode sum32 > gpurun_out/${t}_sweep_sum32.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29583 bench.py --gpus $n > gpurun_out/${t}_bench$n.log 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29584 tools/sweep.py --variants twoshot,twoshot_ce,nccl --mode fast32 > gpurun_out/${t}_sweep_fast32_n2.log 2>&1
