@@ -245,3 +245,23 @@ def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
     for x in xs:
         x.close()
     world.close()
+
+
+def test_size_scaled_chunks_and_parity(cuda):
+    """Big shards get larger chunks (fewer system fences) — the result stays bit-exact."""
+    N, n = 4, (1 << 24) + 12
+    world, trs, xs = build(N, [n, 4096], "fast32", "twoshot", chunk_elems=16384, lr=0.01, momentum=0.9)
+    assert xs[0].layer_plan(0)[0] == 32768  # shard ~4.2 M elements -> >= 128 chunks of 32 K
+    assert xs[0].layer_plan(1)[0] == 16384  # small layer: the configured minimum
+    w = O.seeded_fill(7, n, 0.05).astype(np.float32)
+    for x in xs:
+        x.layer_views[0].copy_(torch.from_numpy(w))
+    grads = [O.seeded_fill(O.derived_seed(1, r), n, 1e-2).astype(np.float32) for r in range(N)]
+    stepped_layer(xs, trs, 0, 0, [[torch.from_numpy(g).cuda()] for g in grads])
+    want, _ = O.exchange_iteration(grads, w, 0.01, "fast32", state=np.zeros(n, np.float32), scale=1.0 / N,
+                                   momentum=0.9, weight_decay=0.0)
+    for r in range(N):
+        assert xs[r].layer_views[0].cpu().numpy().tobytes() == want.tobytes()
+    for x in xs:
+        x.close()
+    world.close()
