@@ -932,6 +932,8 @@ struct pgx_xchg {
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
   bool ce_rs_parts = false;                        // push signals per owner part (signals on ce_rs2)
   bool tma = false;  // TWOSHOT: push / all-gather as TMA bulk copies (PGX_TMA=1; slower fused at N=4, profiles/r1r)
+  bool auto_chunk_tree = false, auto_chunk_nvls = true;  // size-scaled chunks: NVLS yes, tree no (its pipeline
+                                                        // fill grows with the chunk; profiles/r3r)
   bool own_streams = true;                         // false once the caller supplied them
   std::vector<XEvent> done;
   std::vector<XEvent> ready;                       // gradient ready on the launch stream
@@ -1507,6 +1509,8 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   x->world = world_size(w);
   x->dev = world_device(w);
   x->esz = cfg->mode == PGX_MODE_REF64 ? 8 : 4;
+  if (const char* v = getenv("PGX_AUTO_CHUNK_TREE")) x->auto_chunk_tree = atoi(v) != 0;
+  if (const char* v = getenv("PGX_AUTO_CHUNK_NVLS")) x->auto_chunk_nvls = atoi(v) != 0;
   x->seg_model = cfg->seg_base;
   x->seg_rx = cfg->seg_base + 1;
   const int N = x->world;
@@ -1527,10 +1531,11 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     P.variant = cfg->variant ? cfg->variant[l] : PGX_VARIANT_TWOSHOT;
     const bool ch_given = cfg->layer_chunk_elems && cfg->layer_chunk_elems[l];
     uint64_t CH = ch_given ? cfg->layer_chunk_elems[l] : cfg->chunk_elems;
-    if (!ch_given && N > 1 && (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CEP)) {
+    if (!ch_given && N > 1 && P.variant != PGX_VARIANT_TWOSHOT_CE && P.variant != PGX_VARIANT_ONESHOT &&
+        !(P.variant == PGX_VARIANT_TREE && !x->auto_chunk_tree) && !(P.variant == PGX_VARIANT_NVLS && !x->auto_chunk_nvls)) {
       // big shards: chunks of up to 64 K elements (~128 per shard) amortise the system fence
       // that ends every chunk; chunk_elems stays the minimum (profiles/r3e, r3n)
-      const uint64_t target = (P.S + N - 1) / N / 128;
+      const uint64_t target = (P.variant == PGX_VARIANT_TREE ? P.S : (P.S + N - 1) / N) / 128;
       uint64_t c = CH;
       while (c * 2 <= target && c * 2 <= kAutoChunkMax) c *= 2;
       CH = c;
