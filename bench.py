@@ -443,18 +443,23 @@ def pgx_arm(args):
     # ---- timeline: a few traced eager steps, reference CSV schema + overlap ----
     timeline = trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world)
 
-    # ---- per-layer exchange in isolation (same launch, no concurrent backward): every rank,
+    # ---- per-layer exchange in isolation (same launch, no concurrent backward, host enqueue
+    # latency hidden behind a busy kernel so the events bracket device time): every rank,
     # device flag barrier before each, launch -> own part done -> gate on all arrivals.  The
     # dominant layer feeds the roofline; every layer >= 4 MB is reported against NVLink
     # (north star: >= 70 % for such layers).  Runs last: it advances only these layers' epochs. ----
+    HOLD_CYCLES = 300 * 1965  # ~300 us busy kernel ahead of each isolated launch
+
     def isolated(l, reps=10):
         pieces = [torch.randn_like(p) * 1e-3 for p in model.layers()[l][1]]
         ts = []
         for i in range(reps):
             tr.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(xchg.stream):  # hide the host's enqueue latency (device time only)
+                torch.cuda._sleep(HOLD_CYCLES)
             e0.record(xchg.stream)
-            xchg.launch(l, bind.k + i, pieces)
+            xchg.launch(l, bind.k + i, pieces, stream=xchg.stream)
             xchg.join(l, xchg.stream)
             xchg.gate(l, bind.k + i, stream=xchg.stream)
             e1.record(xchg.stream)
@@ -494,6 +499,8 @@ def pgx_arm(args):
             for i in range(12):
                 tr.barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(alt.stream):
+                    torch.cuda._sleep(HOLD_CYCLES)
                 e0.record(alt.stream)
                 alt.launch(l, i, pieces)
                 alt.join(l, alt.stream)

@@ -3,8 +3,9 @@ two-shot vs tree vs NCCL all-reduce (comparison only), fused update on.
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/sweep.py [--max-mb 256] [--ctas 0]
 
-Each point: device flag barrier, then ONE layer exchange (launch + gate) timed with CUDA
-events on the exchange stream, median of --iters after --warmup, max over ranks.
+Each point: device flag barrier, a busy kernel (--hold-us) queued on the stream so the host's
+enqueue latency is hidden, then ONE layer exchange (launch + gate) timed with CUDA events on
+the exchange stream, median of --iters after --warmup, max over ranks.
 busBW convention: 2(N-1)/N * bytes / t.  Prints one JSON line per point on rank 0.
 """
 
@@ -27,6 +28,8 @@ def main():
     ap.add_argument("--max-mb", type=float, default=256)
     ap.add_argument("--min-kb", type=float, default=4)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--hold-us", type=float, default=300.0,
+                    help="busy kernel queued ahead of each timed launch (excludes host enqueue latency; 0 = off)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--chunk", type=int, default=16384)
@@ -64,6 +67,8 @@ def main():
     for x in xs.values():
         x.connect()
 
+    HOLD_CYCLES = int(args.hold_us * 1965)  # SM clock 1965 MHz
+
     def tmax(ms):
         t = torch.tensor([ms])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -76,6 +81,12 @@ def main():
             for it in range(args.warmup + args.iters):
                 tr.barrier()  # device flag barrier: every rank starts together
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                # keep the stream busy while the host enqueues, so the events bracket device
+                # time only (not the Python/ctypes launch latency), for every variant and NCCL
+                hold = torch.cuda.current_stream() if v == "nccl" else xs[v].stream
+                if HOLD_CYCLES:
+                    with torch.cuda.stream(hold):
+                        torch.cuda._sleep(HOLD_CYCLES)
                 if v == "nccl":
                     s = torch.cuda.current_stream()
                     e0.record(s)
@@ -97,7 +108,8 @@ def main():
             bus = 2 * (world - 1) / world * nbytes / (ms / 1e3) / 1e9 if world > 1 else None
             rec = {"n_gpus": world, "variant": v, "bytes": nbytes, "ms": ms, "busbw_gbs": bus,
                    "frac_of_770": bus / 770.0 if bus else None, "ctas": args.ctas, "chunk_elems": args.chunk,
-                   "update": "fused fast32" if v != "nccl" else "none (all-reduce only)"}
+                   "update": ("fused " + args.mode) if v != "nccl" else "none (all-reduce only)",
+                   "hold_us": args.hold_us}
             if rank == 0:
                 print(json.dumps(rec), flush=True)
             out.append(rec)
