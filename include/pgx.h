@@ -185,7 +185,7 @@ int pgx_seeded_fill_f32(uint64_t seed, double scale, float* out, uint64_t n, voi
  *                                  one-sided all-gather into peers' weights;
  *                        ONESHOT = every rank pushes its whole gradient to every
  *                                  peer and updates its own copy (small layers).
- * TREE, TWOSHOT(_CE/_CEP) and ONESHOT are bit-identical to the reference fold order;
+ * TREE, TWOSHOT(_CE/_CEP) and ONESHOT(_LL) are bit-identical to the reference fold order;
  * NVLS reduces in the switch (fast32, tolerance parity). */
 enum pgx_variant {
   PGX_VARIANT_TREE = 0,       /* paper: binomial reduce + master update + broadcast     */
@@ -195,9 +195,11 @@ enum pgx_variant {
                                  multicast weight store; fast32 only, tolerance parity  */
   PGX_VARIANT_ONESHOT = 4,    /* small layers: everyone pushes everything once, every
                                  rank folds (same order) and updates its own copy       */
-  PGX_VARIANT_TWOSHOT_CEP = 5 /* reduce-scatter by the copy engines, then the SM owner
+  PGX_VARIANT_TWOSHOT_CEP = 5,/* reduce-scatter by the copy engines, then the SM owner
                                  kernel (fold + update + all-gather peer stores) on a
                                  capped grid: no per-part copy/event chain            */
+  PGX_VARIANT_ONESHOT_LL = 6  /* small fp32 layers, fence-free: ONESHOT with every value
+                                 carried as an 8-byte {value, epoch} word (2x bytes)  */
 };
 
 typedef struct pgx_xchg_config {

@@ -515,6 +515,131 @@ __global__ void __launch_bounds__(kThreads, 2) k_oneshot(XArgs a) {
   retire(a.queue);
 }
 
+// ============================================================== ONESHOT_LL
+// Latency path for small fp32 layers, fence-free: every element travels as one 8-byte
+// word {value bits, epoch} (LL: the flag rides in the same single-copy-atomic word), four
+// words per 16-byte volatile store.  Every rank writes its whole gradient into each peer's
+// slot [parity][me]; every rank polls its own slots word by word until the epoch matches,
+// folds the N contributions in the binomial order and updates its own copy (as ONESHOT, so
+// bit-identical).  No bar.sync / fence / flag round trip between a store and its use: one
+// NVLink traversal.  Items: C push chunks, then C fold chunks (claimed in order, so every
+// push is claimed before any poll: no deadlock at any residency).  Costs 2x the bytes.
+__device__ __forceinline__ void st_ll4(uint64_t* p, const float* v, int cnt, uint32_t ep) {
+  if (cnt == 4) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(__float_as_uint(v[0])), "r"(ep),
+                 "r"(__float_as_uint(v[1])), "r"(ep)
+                 : "memory");
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p + 2), "r"(__float_as_uint(v[2])), "r"(ep),
+                 "r"(__float_as_uint(v[3])), "r"(ep)
+                 : "memory");
+  } else {
+    for (int i = 0; i < cnt; ++i)
+      asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p + i), "r"(__float_as_uint(v[i])), "r"(ep)
+                   : "memory");
+  }
+}
+
+// Poll cnt words until every epoch field equals ep; bounded like wait_geq.
+__device__ __forceinline__ bool ld_ll4(const uint64_t* p, float* v, int cnt, uint32_t ep, const Status& st) {
+  uint64_t t0 = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    uint32_t d[4], f[4];
+    if (cnt == 4) {
+      asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(d[0]), "=r"(f[0]), "=r"(d[1]), "=r"(f[1])
+                   : "l"(p)
+                   : "memory");
+      asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(d[2]), "=r"(f[2]), "=r"(d[3]), "=r"(f[3])
+                   : "l"(p + 2)
+                   : "memory");
+    } else {
+      for (int i = 0; i < 4; ++i) {
+        if (i < cnt)
+          asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(d[i]), "=r"(f[i]) : "l"(p + i) : "memory");
+        else
+          d[i] = 0, f[i] = ep;
+      }
+    }
+    if (f[0] == ep && f[1] == ep && f[2] == ep && f[3] == ep) {
+      for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(d[i]);
+      return true;
+    }
+    if (spins > 1024) __nanosleep(spins > 65536 ? 1000 : 32);
+    if ((spins & 1023) == 1023) {
+      if (!t0) t0 = globaltimer_ns();
+      if (st.word && *(volatile uint32_t*)st.word) return false;
+      if (st.timeout_ns && globaltimer_ns() - t0 > st.timeout_ns) {
+        if (st.word) atomicCAS(st.word, 0u, (uint32_t)PGX_E_TIMEOUT);
+        return false;
+      }
+    }
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_oneshot_ll(XArgs a) {
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  __shared__ uint32_t s_item;
+  const int me = a.rank;
+  auto slot = [&](int r, int s) {  // rank r's slot [parity][s]: one u64 word per element
+    return reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(a.rx[r]) + (uint64_t)(parity * N + s) * a.sl * 4);
+  };
+  while (true) {
+    uint32_t it = claim(a.queue, &s_item) + a.item_begin;
+    if (it >= a.item_end) break;
+    const bool push = it < a.push_items;
+    const uint32_t c = push ? it : it - a.push_items;
+    const uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
+    const uint64_t nq = (hi - lo + 3) / 4;
+    if (push) {
+      if (N == 1) continue;
+      for (uint64_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        const uint64_t e = lo + q * 4;
+        const int cnt = (int)min((uint64_t)4, hi - e);
+        float g[4];
+        grad_vec<float>(a.g, e, cnt, g);
+#pragma unroll
+        for (int d = 1; d < N; ++d) {
+          const int j = (me + d) % N;
+          st_ll4(slot(j, me) + e, g, cnt, epoch);
+        }
+      }
+    } else {
+      const bool fast = a.mode == PGX_MODE_FAST32;
+      for (uint64_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        const uint64_t e = lo + q * 4;
+        const int cnt = (int)min((uint64_t)4, hi - e);
+        float vals[N][4];
+        bool ok = true;
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          if (s == me)
+            grad_vec<float>(a.g, e, cnt, vals[s]);
+          else
+            ok &= ld_ll4(slot(me, s) + e, vals[s], cnt, epoch, a.st);
+        }
+        if (!ok) break;  // timed out: the host raises TransportError
+        float w[4] = {0.f, 0.f, 0.f, 0.f}, vv[4] = {0.f, 0.f, 0.f, 0.f};
+        float* wp = static_cast<float*>(a.model[me]) + e;
+        if (a.mode != PGX_MODE_SUM32) ld_vec<float>(wp, cnt, w);
+        if (fast) ld_vec<float>(a.v + e, cnt, vv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float col[N];
+#pragma unroll
+          for (int s = 0; s < N; ++s) col[s] = vals[s][k];
+          w[k] = apply_update<float>(w[k], tree_sum<N>(col, AddF32{}), vv[k], a);
+        }
+        st_vec<float>(wp, cnt, w);
+        if (fast) st_vec<float>(a.v + e, cnt, vv);
+      }
+    }
+  }
+  retire(a.queue);
+}
+
 // ============================================================== TREE (paper)
 // Up: chunk c: acc = own + child_0 + child_1 + ... (children ascending, each the
 // child's subtree sum), then to the parent's rx slot, or on rank 0 the update
@@ -932,6 +1057,7 @@ struct pgx_xchg {
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
   bool ce_rs_parts = false;                        // push signals per owner part (signals on ce_rs2)
   bool tma = false;  // TWOSHOT: push / all-gather as TMA bulk copies (PGX_TMA=1; slower fused at N=4, profiles/r1r)
+  bool oneshot_small_chunks = false;  // PGX_ONESHOT_SMALL_CHUNKS=1: measured slower (profiles/r3v)
   bool auto_chunk_tree = false, auto_chunk_nvls = true;  // size-scaled chunks: NVLS yes, tree no (its pipeline
                                                         // fill grows with the chunk; profiles/r3r)
   bool own_streams = true;                         // false once the caller supplied them
@@ -1051,6 +1177,28 @@ void launch_oneshot(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
 #define PGX_CASE(n)                                                        \
   case n:                                                                  \
     k_oneshot<n, T><<<oneshot_grid<n, T>(want, dev), kThreads, 0, s>>>(a); \
+    break;
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
+template <int N>
+int oneshot_ll_grid(int want, int dev) {
+  static int cap[PGX_MAX_RANKS] = {};
+  if (!cap[dev]) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oneshot_ll<N>, kThreads, 0);
+    cap[dev] = std::max(1, per_sm) * sm_count(dev);
+  }
+  return std::max(1, std::min(want, cap[dev]));
+}
+
+void launch_oneshot_ll(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n)                                                            \
+  case n:                                                                      \
+    k_oneshot_ll<n><<<oneshot_ll_grid<n>(want, dev), kThreads, 0, s>>>(a);   \
     break;
     PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
 #undef PGX_CASE
@@ -1511,6 +1659,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   x->esz = cfg->mode == PGX_MODE_REF64 ? 8 : 4;
   if (const char* v = getenv("PGX_AUTO_CHUNK_TREE")) x->auto_chunk_tree = atoi(v) != 0;
   if (const char* v = getenv("PGX_AUTO_CHUNK_NVLS")) x->auto_chunk_nvls = atoi(v) != 0;
+  if (const char* v = getenv("PGX_ONESHOT_SMALL_CHUNKS")) x->oneshot_small_chunks = atoi(v) != 0;
   x->seg_model = cfg->seg_base;
   x->seg_rx = cfg->seg_base + 1;
   const int N = x->world;
@@ -1532,6 +1681,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     const bool ch_given = cfg->layer_chunk_elems && cfg->layer_chunk_elems[l];
     uint64_t CH = ch_given ? cfg->layer_chunk_elems[l] : cfg->chunk_elems;
     if (!ch_given && N > 1 && P.variant != PGX_VARIANT_TWOSHOT_CE && P.variant != PGX_VARIANT_ONESHOT &&
+        P.variant != PGX_VARIANT_ONESHOT_LL &&
         !(P.variant == PGX_VARIANT_TREE && !x->auto_chunk_tree) && !(P.variant == PGX_VARIANT_NVLS && !x->auto_chunk_nvls)) {
       // big shards: chunks of up to 64 K elements (~128 per shard) amortise the system fence
       // that ends every chunk; chunk_elems stays the minimum (profiles/r3e, r3n)
@@ -1591,8 +1741,36 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0)) * own * x->esz +
                     (P.S - own) * x->esz;
 
+    } else if (P.variant == PGX_VARIANT_ONESHOT_LL) {
+      if (x->esz != 4) {
+        delete x;
+        return fail(PGX_E_CONFIG, "layer %d: ONESHOT_LL carries fp32 values (not ref64)", l);
+      }
+      P.sl = align_up(2 * P.S, kAlignElems);  // slot: one 8-byte {value, epoch} word per element
+      if (!ch_given) {  // latency path: spread even small layers over ~one CTA per SM per phase
+        const uint64_t want = align_up((P.S + sms - 1) / sms, 4);
+        CH = std::min<uint64_t>(CH, std::max<uint64_t>(256, want));
+        P.CH = CH;
+      }
+      P.C = (uint32_t)((P.S + CH - 1) / CH);
+      P.K = N;
+      P.rx_off = rxoff;
+      rxoff = align_up(rxoff + 2 * (uint64_t)N * P.sl, kAlignElems);
+      P.rxflag_off = rxfoff;  // no flags: the epoch rides in every word
+      P.push_items = P.C;
+      P.items = 2 * P.C;
+      P.expected = 0;  // each rank updates its own copy
+      P.grid = (int)std::min<uint64_t>(P.items, cap);
+      P.nvlink_bytes = 2ull * (N - 1) * P.S * x->esz;
+      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0)) * P.S * x->esz +
+                    (uint64_t)(N - 1) * P.S * x->esz;
     } else if (P.variant == PGX_VARIANT_ONESHOT) {
       P.sl = align_up(P.S, kAlignElems);  // slot stride: every peer's whole gradient
+      if (!ch_given && x->oneshot_small_chunks) {  // latency: more, smaller chunks in parallel
+        const uint64_t want = align_up((P.S + sms - 1) / sms, 4);
+        CH = std::min<uint64_t>(CH, std::max<uint64_t>(1024, want));
+        P.CH = CH;
+      }
       P.C = (uint32_t)((P.S + CH - 1) / CH);
       P.K = N;
       P.rx_off = rxoff;
@@ -1787,6 +1965,20 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
   int prev;
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
+  if (P.variant == PGX_VARIANT_ONESHOT_LL) {
+    xrecord(x->ready[l], s);
+    a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
+    a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
+    if (a.item_end > a.item_begin) {
+      ++x->launches;
+      launch_oneshot_ll(x->world, (int)std::min<uint32_t>(a.item_end - a.item_begin, (uint32_t)P.grid), x->dev, s, a);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = xrecord(x->done[l], s);
+    if (prev != x->dev) cudaSetDevice(prev);
+    if (e != cudaSuccess) return fail(PGX_E_CUDA, "exchange launch failed: %s", cudaGetErrorString(e));
+    return PGX_OK;
+  }
   if (P.variant == PGX_VARIANT_ONESHOT) {
     xrecord(x->ready[l], s);
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;

@@ -24,17 +24,20 @@ from . import _lib
 from .errors import ConfigError, ShapeError
 
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
-            "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP}
+            "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP,
+            "oneshot_ll": _lib.VARIANT_ONESHOT_LL}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 
 def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20,
-                   oneshot_below: int | None = None, large: str = "ce") -> str:
+                   oneshot_below: int | None = None, large: str = "ce", ll_below: int = 0) -> str:
     """Layer-size policy (measured, profiles/r1*_sweep*): the smallest layers are pure
     latency and take the one-shot exchange (one NVLink hop); mid-size layers the SM
     two-shot kernel; layers of `ce_from` elements or more move their shards with the copy
     engines, which do not take SMs away from the backward kernels they overlap with.
-    `tree_below` optionally keeps the paper's tree for the smallest layers.  large="sm"
+    `tree_below` optionally keeps the paper's tree for the smallest layers.  `ll_below`
+    (fp32 modes; DeviceExchange passes 64 K elements) sends the smallest layers as LL words
+    (profiles/r3v: 14–21 µs up to 256 KB at N=4, NCCL 17–23).  large="sm"
     keeps the SM two-shot for the large layers too (run with a CTA cap and big chunks,
     see DeviceExchange `large_ctas`); large="cep" moves the reduce-scatter by copy engine
     and runs fold + update + all-gather as the SM owner kernel on a capped grid."""
@@ -42,6 +45,8 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
         oneshot_below = (1 << 20) // max(world, 1)  # N=4: 1 MB layers (profiles/r2b_sweep_n4)
     if world > 1 and elems < tree_below:
         return "tree"
+    if world > 1 and elems <= ll_below:  # fence-free LL words: lowest latency up to ~256 KB
+        return "oneshot_ll"
     if world > 1 and elems < oneshot_below:
         return "oneshot"
     if world > 1 and elems >= ce_from:
@@ -71,7 +76,8 @@ class DeviceExchange:
         self.layer_elems = [int(n) for n in layer_elems]
         L = len(self.layer_elems)
         if isinstance(variant, str) and variant == "auto":
-            variants = [choose_variant(n, self.world, tree_below, ce_from=large_from, large=large)
+            ll = (1 << 16) if mode != "ref64" else 0
+            variants = [choose_variant(n, self.world, tree_below, ce_from=large_from, large=large, ll_below=ll)
                         for n in self.layer_elems]
         elif isinstance(variant, str):
             variants = [variant] * L

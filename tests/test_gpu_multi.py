@@ -108,7 +108,7 @@ def _ngpu():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot")
+@pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll")
                                           for m in ("ref32", "fast32")]
                          + [("nvls", "fast32")])
 def test_concurrent_exchange_matches_oracle(variant, mode):
@@ -274,7 +274,7 @@ def _model_worker(rank, world, port, which, variant, gate, q):
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("which", ["lenet", "cifar10_quick"])
 @pytest.mark.parametrize("variant,gate", [("twoshot", "layer"), ("twoshot_ce", "layer"), ("twoshot_cep", "layer"), ("tree", "layer"),
-                                          ("twoshot_ce", "model"), ("nvls", "layer"), ("oneshot", "layer")])
+                                          ("twoshot_ce", "model"), ("nvls", "layer"), ("oneshot", "layer"), ("oneshot_ll", "layer")])
 def test_real_models_match_oracle(which, variant, gate):
     world = 2 if which == "lenet" else min(4, _ngpu())
     out = _spawn(_model_worker, world, which, variant, gate)
@@ -322,7 +322,7 @@ def _fault_worker(rank, world, port, variant, q):
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep"])
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot_ll"])
 def test_dead_peer_surfaces_as_transport_error(variant):
     out = _spawn(_fault_worker, 2, variant)
     assert out[0][1].startswith("TransportError"), out

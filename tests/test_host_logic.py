@@ -142,3 +142,19 @@ def test_oracle_children_match_package_tree():
         t = build_reduction_tree(s)
         for r in range(s):
             assert t.children[r] == O.tree_children(r, s)
+
+
+def test_variant_policy():
+    """Layer-size policy of the auto exchange (profiles/r3v, r3t, r3p)."""
+    from paper_1706_00095_b200.exchange import choose_variant
+
+    ll = 1 << 16
+    assert choose_variant(35_000, 4, ll_below=ll) == "oneshot_ll"        # AlexNet conv1
+    assert choose_variant(35_000, 4) == "oneshot"                         # ref64: no LL
+    assert choose_variant(200_000, 4, ll_below=ll) == "oneshot"           # < 1M/N elements
+    assert choose_variant(500_000, 4, ll_below=ll) == "twoshot"
+    assert choose_variant(37_752_832, 4, ll_below=ll) == "twoshot_ce"     # fc6
+    assert choose_variant(37_752_832, 4, large="sm") == "twoshot"
+    assert choose_variant(37_752_832, 4, large="cep") == "twoshot_cep"
+    assert choose_variant(37_752_832, 1, ll_below=ll) == "twoshot"        # N=1: the fused update
+    assert choose_variant(1000, 8, tree_below=4096, ll_below=ll) == "tree"
