@@ -254,7 +254,7 @@ def test_size_scaled_chunks_and_parity(cuda):
     N, n = 4, (1 << 24) + 12
     world, trs, xs = build(N, [n, 4096], "fast32", "twoshot", chunk_elems=16384, lr=0.01, momentum=0.9)
     assert xs[0].layer_plan(0)[0] == 32768  # shard ~4.2 M elements -> >= 128 chunks of 32 K
-    assert xs[0].layer_plan(1)[0] == 16384  # small layer: the configured minimum
+    assert xs[0].layer_plan(1)[0] == 8192  # small shard (<= 256 K elements): half chunks
     w = O.seeded_fill(7, n, 0.05).astype(np.float32)
     for x in xs:
         x.layer_views[0].copy_(torch.from_numpy(w))
