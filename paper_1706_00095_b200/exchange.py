@@ -317,6 +317,7 @@ class ModuleBinding:
                 self._handles.append(p.register_post_accumulate_grad_hook(self._make_hook(l)))
             self._handles.append(mod.register_forward_pre_hook(self._make_gate(l)))
         self.gpu_launches = 0
+        self._capture_keep: list = []   # gradients read by captured exchanges (graph lifetime)
         self.timed_layers: set = set()   # layers whose launches are bracketed by CUDA events
         self._tstream = None
         self.trace = None                # list -> record (iteration, layer, ready_event, done_event)
@@ -348,6 +349,11 @@ class ModuleBinding:
                 e1 = torch.cuda.Event(enable_timing=True, external=ext)
                 e0.record(xs)
             self.x.launch(l, self.k, pieces, stream=xs)
+            if torch.cuda.is_current_stream_capturing():
+                # record_stream does not order frees inside a capture: without a reference the
+                # allocator would hand this gradient's memory to the next layer's backward in
+                # the same graph, which then overwrites it while the exchange still reads it
+                self._capture_keep.extend(pieces)
             if timed:  # end = this rank's part done on every internal stream (copy-engine variants too)
                 if self._tstream is None:
                     self._tstream = torch.cuda.Stream(device=self.x.tr.device)
@@ -415,3 +421,4 @@ class ModuleBinding:
     def remove(self) -> None:
         for h in self._handles:
             h.remove()
+        self._capture_keep.clear()

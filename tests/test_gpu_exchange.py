@@ -175,7 +175,7 @@ class _FixedGrad(torch.nn.Module):
         return (self.weight * self.c).sum() + (self.bias * self.d).sum()
 
 
-@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep"])
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll"])
 @pytest.mark.parametrize("gate", ["layer", "model"])
 def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     """A captured training step (device iteration counter) applies exactly the oracle update."""

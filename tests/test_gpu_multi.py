@@ -327,3 +327,118 @@ def test_dead_peer_surfaces_as_transport_error(variant):
     out = _spawn(_fault_worker, 2, variant)
     assert out[0][1].startswith("TransportError"), out
     assert out[1][1] == "no error", out
+
+
+def _graph_worker(rank, world, port, variant, gate, use_graph, q):
+    """Several layers, one process per GPU, the whole step captured once as a CUDA graph
+    (device iteration counter) and replayed: each rank's gradient is a fixed per-rank
+    constant (loss = sum(w*c_r) + sum(b*d_r)), so after the replays every rank must hold
+    exactly the oracle's weights for the N-rank exchange."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(rank)
+    from oracle import pipesgd_oracle as O
+    from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
+    from paper_1706_00095_b200.transport import DistTransport
+
+    class Fixed(torch.nn.Module):
+        def __init__(self, n, r):
+            super().__init__()
+            gw = torch.Generator().manual_seed(5 + n)  # same initial weights on every rank
+            self.weight = torch.nn.Parameter(torch.randn(n, generator=gw).cuda())
+            self.bias = torch.nn.Parameter(torch.randn(7, generator=gw).cuda())
+            gg = torch.Generator().manual_seed(1000 * r + n)  # per-rank gradients
+            self.c = (torch.randn(n, generator=gg) * 1e-2).cuda()
+            self.d = (torch.randn(7, generator=gg) * 1e-2).cuda()
+
+        def forward(self, x):
+            return x + (self.weight * self.c).sum() + (self.bias * self.d).sum()
+
+    try:
+        sizes = [3000, 70000, 400000, 1500000]  # LL / one-shot / two-shot / copy-engine sizes at N=4
+        mods = [Fixed(n, rank) for n in sizes]
+        layers = [(m, [m.weight, m.bias]) for m in mods]
+        tr = DistTransport(rank, world, rank, timeout_s=20.0)
+        x = DeviceExchange(tr, [n + 7 for n in sizes], mode="fast32", variant=variant, lr=0.05, momentum=0.9,
+                           weight_decay=1e-3)
+        bind = ModuleBinding(x, layers, gate=gate)
+        tr.barrier()
+        x.connect()
+
+        def step():
+            y = torch.zeros((), device="cuda")
+            for m in mods:
+                y = m(y)
+            y.backward()
+            bind.step_done()
+
+        w0 = [torch.cat([m.weight.detach(), m.bias.detach()]).cpu().numpy() for m in mods]
+        for _ in range(2):
+            step()
+        bind.drain()
+        torch.cuda.synchronize()
+        if use_graph:
+            x.set_device_iteration(True, bind.k - 1)
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap), torch.cuda.graph(graph, stream=cap):
+                bind.begin_step()
+                step()
+                bind.drain()
+            torch.cuda.current_stream().wait_stream(cap)
+            for _ in range(3):
+                graph.replay()
+            bind.wait_current()
+        else:
+            for _ in range(3):
+                step()
+            bind.drain()
+        torch.cuda.synchronize()
+        # oracle: 5 exchanges (2 eager steps + 3 replays; capturing runs nothing) of every
+        # rank's fixed gradient
+        grads = []
+        for n in sizes:
+            per = []
+            for r in range(world):
+                gg = torch.Generator().manual_seed(1000 * r + n)
+                c = (torch.randn(n, generator=gg) * 1e-2).numpy()
+                d = (torch.randn(7, generator=gg) * 1e-2).numpy()
+                per.append(np.concatenate([c, d]).astype(np.float32))
+            grads.append(per)
+        bad = []
+        for l, n in enumerate(sizes):
+            w, v = w0[l].copy(), np.zeros_like(w0[l])
+            for _ in range(5):
+                w, v = O.exchange_iteration(grads[l], w, 0.05, "fast32", state=v, scale=1.0 / world,
+                                            momentum=0.9, weight_decay=1e-3)
+            got = x.layer_views[l].cpu().numpy()
+            if got.tobytes() != w.tobytes():
+                bad.append((l, float(np.max(np.abs(got - w)))))
+        q.put((rank, bad, tr.device_status()))
+        bind.remove()
+        x.close()
+        tr.close()
+    except Exception as exc:  # noqa: BLE001
+        q.put((rank, repr(exc), -1))
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("variant,gate", [("auto", "layer"), ("auto", "model"), ("twoshot", "layer"),
+                                          ("twoshot_ce", "layer"), ("twoshot_cep", "model"), ("tree", "layer"),
+                                          ("oneshot", "layer"), ("oneshot_ll", "model")])
+def test_graph_replay_multi_gpu_matches_oracle(variant, gate):
+    out = _spawn(_graph_worker, _ngpu(), variant, gate, True)
+    for rank, bad, status in out:
+        assert bad == [] and status == 0, (rank, bad, status)
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("variant", ["auto", "twoshot"])
+def test_eager_chain_multi_gpu_matches_oracle(variant):
+    out = _spawn(_graph_worker, _ngpu(), variant, "layer", False)
+    for rank, bad, status in out:
+        assert bad == [] and status == 0, (rank, bad, status)
