@@ -267,3 +267,73 @@ def test_size_scaled_chunks_and_parity(cuda):
     for x in xs:
         x.close()
     world.close()
+
+
+class _Chain(torch.nn.Module):
+    """y = x + sum(w*c) + sum(b*d): chained in a model, every layer's gradient is exactly
+    (c, d), and later layers' backward allocations would reuse freed gradient memory."""
+
+    def __init__(self, n, seed):
+        super().__init__()
+        gen = torch.Generator().manual_seed(seed)
+        self.weight = torch.nn.Parameter(torch.randn(n, generator=gen).cuda())
+        self.bias = torch.nn.Parameter(torch.randn(7, generator=gen).cuda())
+        self.c = (torch.randn(n, generator=gen) * 1e-2).cuda()
+        self.d = (torch.randn(7, generator=gen) * 1e-2).cuda()
+
+    def forward(self, x):
+        return x + (self.weight * self.c).sum() + (self.bias * self.d).sum()
+
+
+@pytest.mark.parametrize("gate", ["layer", "model"])
+def test_cuda_graph_multi_layer_single_gpu(cuda, gate):
+    """Several layers in one captured step on one GPU: each layer's fused update must read
+    its own gradient, not memory a later layer's backward reused (graph-lifetime keep)."""
+    from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
+    from paper_1706_00095_b200.transport import LocalWorld
+
+    sizes = [3000, 70000, 400000, 1500000]
+    mods = [_Chain(n, 11 + i) for i, n in enumerate(sizes)]
+    layers = [(m, [m.weight, m.bias]) for m in mods]
+    world = LocalWorld(1, inline=False)
+    tr = world.transport(0)
+    x = DeviceExchange(tr, [n + 7 for n in sizes], mode="fast32", variant="auto", lr=0.05, momentum=0.9,
+                       weight_decay=1e-3)
+    x.connect()
+    bind = ModuleBinding(x, layers, gate=gate)
+    w = [torch.cat([m.weight.detach(), m.bias.detach()]).cpu().numpy() for m in mods]
+    g = [torch.cat([m.c, m.d]).cpu().numpy() for m in mods]
+    v = [np.zeros_like(a) for a in w]
+
+    def step():
+        y = torch.zeros((), device="cuda")
+        for m in mods:
+            y = m(y)
+        y.backward()
+        bind.step_done()
+
+    for _ in range(2):
+        step()
+    bind.drain()
+    torch.cuda.synchronize()
+    x.set_device_iteration(True, bind.k - 1)
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap), torch.cuda.graph(graph, stream=cap):
+        bind.begin_step()
+        step()
+        bind.drain()
+    torch.cuda.current_stream().wait_stream(cap)
+    for _ in range(3):
+        graph.replay()
+    bind.wait_current()
+    torch.cuda.synchronize()
+    for l in range(len(sizes)):
+        for _ in range(5):  # 2 eager steps + 3 replays (capturing runs nothing)
+            w[l], v[l] = O.fast32_update(w[l], v[l], g[l], 1.0, 0.05, 0.9, 1e-3)
+        assert x.layer_views[l].cpu().numpy().tobytes() == w[l].tobytes(), f"layer {l}"
+    assert tr.device_status() == 0
+    bind.remove()
+    x.close()
+    world.close()
