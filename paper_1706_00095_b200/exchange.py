@@ -131,6 +131,7 @@ class DeviceExchange:
             # so their CTAs fill gaps instead of pre-empting the backward kernels
             self.stream_low = torch.cuda.Stream(device=transport.device, priority=0)
         self.low_priority_from = low_priority_from
+        self._capture_keep: list = []  # gradient pieces read by captured launches
         self.connected = False
         self.device_iteration = False
         self.launches = 0
@@ -227,6 +228,11 @@ class DeviceExchange:
                 p.record_stream(st)
                 for s in self.internal_streams:
                     p.record_stream(s)
+        else:
+            # inside a capture record_stream does not order frees: a piece freed now would be
+            # handed to a later allocation of the same graph while the replayed exchange still
+            # reads it, so captured pieces live as long as this exchange (the graph's memory)
+            self._capture_keep.extend(pieces)
         self.launches += 1
 
     def set_device_iteration(self, enable: bool, current: int) -> None:
@@ -274,6 +280,7 @@ class DeviceExchange:
             torch.cuda.synchronize(self.tr.device)
             _lib.call("pgx_xchg_destroy", self.handle)
             self.handle = None
+            self._capture_keep.clear()
 
 
 class ModuleBinding:
@@ -317,7 +324,6 @@ class ModuleBinding:
                 self._handles.append(p.register_post_accumulate_grad_hook(self._make_hook(l)))
             self._handles.append(mod.register_forward_pre_hook(self._make_gate(l)))
         self.gpu_launches = 0
-        self._capture_keep: list = []   # gradients read by captured exchanges (graph lifetime)
         self.timed_layers: set = set()   # layers whose launches are bracketed by CUDA events
         self._tstream = None
         self.trace = None                # list -> record (iteration, layer, ready_event, done_event)
@@ -348,12 +354,7 @@ class ModuleBinding:
                 e0 = torch.cuda.Event(enable_timing=True, external=ext)
                 e1 = torch.cuda.Event(enable_timing=True, external=ext)
                 e0.record(xs)
-            self.x.launch(l, self.k, pieces, stream=xs)
-            if torch.cuda.is_current_stream_capturing():
-                # record_stream does not order frees inside a capture: without a reference the
-                # allocator would hand this gradient's memory to the next layer's backward in
-                # the same graph, which then overwrites it while the exchange still reads it
-                self._capture_keep.extend(pieces)
+            self.x.launch(l, self.k, pieces, stream=xs)  # keeps captured pieces alive (graph lifetime)
             if timed:  # end = this rank's part done on every internal stream (copy-engine variants too)
                 if self._tstream is None:
                     self._tstream = torch.cuda.Stream(device=self.x.tr.device)
@@ -421,4 +422,3 @@ class ModuleBinding:
     def remove(self) -> None:
         for h in self._handles:
             h.remove()
-        self._capture_keep.clear()
