@@ -55,3 +55,28 @@ def test_product_path_never_imports_the_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "from oracle" not in src and "import oracle" not in src
+
+
+def test_header_constants_match_the_python_mirror():
+    """Enum values and limits in include/pgx.h are what _lib / exchange / errors use."""
+    import re
+
+    from paper_1706_00095_b200 import errors
+    from paper_1706_00095_b200.exchange import MODES, VARIANTS
+
+    text = open(os.path.join(os.path.dirname(_lib.LIB_PATH), "..", "include", "pgx.h")).read()
+    enum = {m.group(1): int(m.group(2)) for m in re.finditer(r"\b(PGX_[A-Z0-9_]+)\s*=\s*(\d+)", text)}
+    define = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(PGX_[A-Z0-9_]+)\s+(\d+)", text)}
+    for name, val in VARIANTS.items():
+        assert enum["PGX_VARIANT_" + name.upper()] == val, name
+    for name, val in MODES.items():
+        assert enum["PGX_MODE_" + name.upper()] == val, name
+    assert define["PGX_XCHG_STREAMS"] == _lib.XCHG_STREAMS
+    assert define["PGX_CKPT_MAX_LAYERS"] == _lib.CKPT_MAX_LAYERS
+    assert define["PGX_MAX_RANKS"] == _lib.MAX_RANKS
+    assert define["PGX_MAX_PIECES"] == _lib.MAX_PIECES
+    assert define["PGX_IPC_HANDLE_BYTES"] == _lib.IPC_HANDLE_BYTES
+    status = {k[len("PGX_E_"):]: v for k, v in enum.items() if k.startswith("PGX_E_")}
+    assert set(errors.STATUS_CLASSES) == set(status.values())
+    assert errors.STATUS_CLASSES[status["FORMAT"]] is errors.FormatError
+    assert errors.STATUS_CLASSES[status["TIMEOUT"]] is errors.TransportError
