@@ -458,6 +458,8 @@ def pgx_arm(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             with torch.cuda.stream(xchg.stream):  # hide the host's enqueue latency (device time only)
                 torch.cuda._sleep(HOLD_CYCLES)
+            if world > 1:
+                tr.barrier_async(xchg.stream)  # ranks start within one flag round trip
             e0.record(xchg.stream)
             xchg.launch(l, bind.k + i, pieces, stream=xchg.stream)
             xchg.join(l, xchg.stream)
@@ -501,6 +503,7 @@ def pgx_arm(args):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 with torch.cuda.stream(alt.stream):
                     torch.cuda._sleep(HOLD_CYCLES)
+                tr.barrier_async(alt.stream)
                 e0.record(alt.stream)
                 alt.launch(l, i, pieces)
                 alt.join(l, alt.stream)

@@ -113,6 +113,9 @@ int pgx_ticket_release(void* ticket);
 /* Device flag barrier over CONTROL_SEGMENT (tcp.py:229-269 analog). Only for
  * ranks on distinct GPUs; host-stepped single-GPU worlds barrier on the host. */
 int pgx_barrier(pgx_world* w, void* stream, double timeout_s);
+/* The same device barrier enqueued on `stream` without waiting for it on the host (ranks
+ * leave it within one flag round trip of each other: used to align timed regions). */
+int pgx_barrier_async(pgx_world* w, void* stream, double timeout_s);
 
 /* ------------------------------------------------------------ arithmetic
  * buffer_axpy (buffers.py:69-74): y := y + (alpha*x), two roundings. */

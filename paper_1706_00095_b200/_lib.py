@@ -77,6 +77,7 @@ SIGNATURES = {
     "pgx_ticket_wait": [vp, C.c_double],
     "pgx_ticket_release": [vp],
     "pgx_barrier": [vp, vp, C.c_double],
+    "pgx_barrier_async": [vp, vp, C.c_double],
     "pgx_axpy_f64": [C.c_double, vp, vp, u64, vp],
     "pgx_axpy_f32": [C.c_float, vp, vp, u64, vp],
     "pgx_master_update_f64": [vp, vp, C.c_double, vp, u64, vp],

@@ -446,8 +446,24 @@ int pgx_ticket_release(void* t) {
   return PGX_OK;
 }
 
+static int launch_barrier(pgx_world* w, void* stream, double timeout_s);
+
 int pgx_barrier(pgx_world* w, void* stream, double timeout_s) {
   if (w->world == 1) return PGX_OK;
+  int rc = launch_barrier(w, stream, timeout_s);
+  if (rc) return rc;
+  PGX_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (*(volatile uint32_t*)w->status_host)
+    return fail(PGX_E_TIMEOUT, "barrier did not complete within %g s", timeout_s);
+  return PGX_OK;
+}
+
+int pgx_barrier_async(pgx_world* w, void* stream, double timeout_s) {
+  if (w->world == 1) return PGX_OK;
+  return launch_barrier(w, stream, timeout_s);
+}
+
+static int launch_barrier(pgx_world* w, void* stream, double timeout_s) {
   BarrierArgs a;
   for (int j = 0; j < w->world; ++j) {
     SegRec* s = find_seg(w, j, PGX_CONTROL_SEGMENT);
@@ -459,9 +475,6 @@ int pgx_barrier(pgx_world* w, void* stream, double timeout_s) {
   DeviceGuard g(w->device);
   k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(a, a.peer_ctrl[w->rank], w->rank, w->world, epoch, st);
   PGX_LAUNCH_CHECK();
-  PGX_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-  if (*(volatile uint32_t*)w->status_host)
-    return fail(PGX_E_TIMEOUT, "barrier did not complete within %g s", timeout_s);
   return PGX_OK;
 }
 

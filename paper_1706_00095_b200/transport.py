@@ -444,3 +444,9 @@ class DistTransport(CudaTransport):
         if not self._connected:
             self.connect()
         _lib.call("pgx_barrier", self.handle, self.stream.cuda_stream, float(self._timeout))
+
+    def barrier_async(self, stream) -> None:
+        """Enqueue the device flag barrier on `stream` without waiting on the host: every
+        rank's stream leaves it within one flag round trip (aligns timed regions).  Not
+        counted in barrier_calls (measurement only, never on the exchange path)."""
+        _lib.call("pgx_barrier_async", self.handle, stream.cuda_stream, float(self._timeout))

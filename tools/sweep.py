@@ -28,6 +28,9 @@ def main():
     ap.add_argument("--max-mb", type=float, default=256)
     ap.add_argument("--min-kb", type=float, default=4)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--align", type=int, default=1,
+                    help="1: a device flag barrier on the timed stream right before the start event, so "
+                         "ranks start within one flag round trip (host wake-up skew excluded; NCCL too)")
     ap.add_argument("--hold-us", type=float, default=300.0,
                     help="busy kernel queued ahead of each timed launch (excludes host enqueue latency; 0 = off)")
     ap.add_argument("--warmup", type=int, default=5)
@@ -87,6 +90,8 @@ def main():
                 if HOLD_CYCLES:
                     with torch.cuda.stream(hold):
                         torch.cuda._sleep(HOLD_CYCLES)
+                if args.align and world > 1:  # device barrier right before e0: no start skew
+                    tr.barrier_async(hold)
                 if v == "nccl":
                     s = torch.cuda.current_stream()
                     e0.record(s)
@@ -109,7 +114,7 @@ def main():
             rec = {"n_gpus": world, "variant": v, "bytes": nbytes, "ms": ms, "busbw_gbs": bus,
                    "frac_of_770": bus / 770.0 if bus else None, "ctas": args.ctas, "chunk_elems": args.chunk,
                    "update": ("fused " + args.mode) if v != "nccl" else "none (all-reduce only)",
-                   "hold_us": args.hold_us}
+                   "hold_us": args.hold_us, "aligned_start": bool(args.align)}
             if rank == 0:
                 print(json.dumps(rec), flush=True)
             out.append(rec)
