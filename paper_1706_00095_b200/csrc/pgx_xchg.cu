@@ -9,14 +9,24 @@
 // system-scope release, and the waits are device-side acquire spins, so the host
 // never polls.
 //
-//   TREE     the paper's schedule: chunk-pipelined binomial reduce to rank 0,
-//            fused update on rank 0, chunk-pipelined broadcast down the edges.
-//   TWOSHOT  every rank pushes shard j of its gradient into owner j's receive
-//            slot; owner j folds the N contributions in the SAME binomial order
-//            (tree_sum<N>), applies the fused update, and stores the updated
-//            shard straight into every peer's weight buffer.
+//   TREE         the paper's schedule: chunk-pipelined binomial reduce to rank 0,
+//                fused update on rank 0, chunk-pipelined broadcast down the edges.
+//   TWOSHOT      every rank pushes shard j of its gradient into owner j's receive
+//                slot; owner j folds the N contributions in the SAME binomial order
+//                (tree_sum<N>), applies the fused update, and stores the updated
+//                shard straight into every peer's weight buffer.
+//   TWOSHOT_CE   the same schedule with the shards moved by copy engines
+//                (cudaMemcpyAsync + k_signal); the SM kernel only folds + updates.
+//   TWOSHOT_CEP  copy-engine reduce-scatter, SM owner kernel (fold + update +
+//                all-gather stores) on a capped grid.
+//   ONESHOT      small layers: everyone pushes everything once, every rank folds
+//                and updates its own copy; ONESHOT_LL does it fence-free with
+//                {value, epoch} words.
+//   NVLS         multicast objects: switch-side reduce (multimem.ld_reduce) and
+//                broadcast (multimem.st); fp32 tolerance parity.
 //
-// Both give bit-identical weights to the reference fold order.  Work is split
+// All but NVLS give bit-identical weights to the reference fold order; modes
+// ref64 / ref32 / fast32 / sum32 (update off) select the per-element update.  Work is split
 // into chunks (the notification unit, runtime.py:209-222) claimed through a
 // per-layer atomic queue: every non-waiting push chunk is claimed before any
 // waiting chunk, so a launch makes progress with any number of resident CTAs.
