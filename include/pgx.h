@@ -285,6 +285,10 @@ int pgx_xchg_layer_bytes(pgx_xchg* x, int layer, uint64_t* nvlink_out_bytes,
 /* The plan a layer runs with: effective chunk elements (notification granularity) and
  * CTAs of its exchange kernel launch. */
 int pgx_xchg_layer_plan(pgx_xchg* x, int layer, uint64_t* chunk_elems_out, int* ctas_out);
+/* Debug timeline: when `device_buffer` (u64 [items][4]) is non-NULL, instrumented kernels
+ * (ONESHOT) stamp each work item's claim / mid / end globaltimer ns and SM id into it.
+ * NULL turns it off (the default: one predicated-off branch per item). */
+int pgx_xchg_set_trace(pgx_xchg* x, void* device_buffer);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,7 @@ SIGNATURES = {
     "pgx_xchg_nvls_bind": [vp],
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
     "pgx_xchg_layer_plan": [vp, i32, P(u64), P(i32)],
+    "pgx_xchg_set_trace": [vp, vp],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],
     "pgx_xchg_set_streams": [vp, P(vp), i32],

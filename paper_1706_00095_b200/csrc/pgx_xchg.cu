@@ -91,6 +91,7 @@ struct XArgs {
   uint32_t item_begin, item_end;       // claimed range (phase selection)
   uint64_t olo, ohi;                   // TWOSHOT_CE owner sub-range (ohi == 0: the whole shard)
   int single_buffer;                   // rx parity fixed at 0 (TWOSHOT_CEP: host-addressed copies)
+  unsigned long long* trace;           // debug: per-item globaltimer stamps (pgx_xchg_set_trace) or null
   const uint32_t* iter;                // device iteration counter (graph mode) or null
   double lr;
   float scale, mu, wd;
@@ -475,13 +476,23 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
   retire(a.queue);
 }
 
+// Debug timeline (pgx_xchg_set_trace): item `it` -> [claim, mid, end, smid], thread 0 only.
+__device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slot) {
+  if (a.trace && threadIdx.x == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.trace[(uint64_t)it * 4 + slot] = globaltimer_ns();
+    a.trace[(uint64_t)it * 4 + 3] = sm;
+  }
+}
+
 // ============================================================== ONESHOT
 // Small layers are latency-bound: every rank pushes its whole gradient to every peer
 // (one NVLink traversal), then folds all N contributions in the same binomial order
 // and applies the update to its own copy.  No all-gather, no second hop; bit-identical
 // to the other variants because every rank evaluates the same expression.
 template <int N, class T>
-__global__ void __launch_bounds__(kThreads, 2) k_oneshot(XArgs a) {
+__global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && N >= 3 && N <= 4) ? 1 : 2) k_oneshot(XArgs a) {
   constexpr int W = VecT<T>::W;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
@@ -491,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_oneshot(XArgs a) {
   while (true) {
     uint32_t it = claim(a.queue, &s_item) + a.item_begin;
     if (it >= a.item_end) break;
+    trace_stamp(a, it, 0);
     if (N > 1 && it < a.push_items) {
       constexpr int NP = N > 1 ? N - 1 : 1;
       uint32_t c = it / NP;
@@ -506,7 +518,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_oneshot(XArgs a) {
         grad_vec<T>(a.g, e, cnt, buf);
         st_vec<T>(dst + q * W, cnt, buf);
       }
+      trace_stamp(a, it, 1);
       cta_release_flag(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
+      trace_stamp(a, it, 2);
     } else {
       uint32_t c = it - a.push_items;
       uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
@@ -516,10 +530,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_oneshot(XArgs a) {
       }
       __syncthreads();
       cta_wait_flags(s_flags, N - 1, epoch, a.st);
+      trace_stamp(a, it, 1);
       const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + lo;
       uint64_t nvec = (hi - lo + W - 1) / W;
-      for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += blockDim.x)
-        owner_vectors<N, T, 1, false>(a, rxb, lo, hi, q0, nvec);
+      // fp32 and N <= 4: two vectors per thread in flight (the fold is load-latency bound;
+      // profiles/r4i: 8 us of a 1 MB exchange at N=4 with one)
+      constexpr int UO = (sizeof(T) == 4 && N <= 4) ? 2 : 1;
+      for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)UO * blockDim.x)
+        owner_vectors<N, T, UO, false>(a, rxb, lo, hi, q0, nvec);
+      __syncthreads();
+      trace_stamp(a, it, 2);
     }
   }
   retire(a.queue);
@@ -1078,6 +1098,7 @@ struct pgx_xchg {
   std::vector<std::vector<XEvent>> part_ev;        // TWOSHOT_CE owner parts ready for their all-gather
   std::vector<std::vector<XEvent>> rs_part_ev;     // TWOSHOT_CE push parts copied (per-part signals)
   uint32_t* iter_dev = nullptr;                    // device iteration counter (graph mode)
+  unsigned long long* trace = nullptr;             // debug timeline buffer (pgx_xchg_set_trace)
   bool device_iter = false;
   uint32_t ownerflag_base = 0;                     // mflags index of [layer][owner] arrival flags
   GateEntry* gate_table = nullptr;                 // device: every layer's arrival flags
@@ -1133,6 +1154,7 @@ XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
   a.mode = x->cfg.mode;
   a.st = world_status(x->w);
   a.iter = x->device_iter ? x->iter_dev : nullptr;
+  a.trace = x->trace;
   return a;
 }
 
@@ -2211,6 +2233,11 @@ int pgx_xchg_layer_bytes(pgx_xchg* x, int l, uint64_t* nvl, uint64_t* hbm) {
   if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
   if (nvl) *nvl = x->L[l].nvlink_bytes;
   if (hbm) *hbm = x->L[l].hbm_bytes;
+  return PGX_OK;
+}
+
+int pgx_xchg_set_trace(pgx_xchg* x, void* device_buffer) {
+  x->trace = static_cast<unsigned long long*>(device_buffer);
   return PGX_OK;
 }
 
