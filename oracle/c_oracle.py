@@ -91,7 +91,7 @@ class ExchangeWorld:
         self._e = (C.c_uint64 * L)(*self.elems)
 
     def iteration(self, mode="fast32", lr=0.01, scale=None, mu=0.9, wd=5e-4, threads=1):
-        m = {"ref32": 1, "fast32": 2}[mode]
+        m = {"ref32": 1, "fast32": 2, "sum32": 3}[mode]
         sc = 1.0 / self.world if scale is None else scale
         lib().oracle_exchange_iteration(self.world, len(self.elems), self._e, C.cast(self._g, C.c_void_p),
                                         C.cast(self._w, C.c_void_p), C.cast(self._v, C.c_void_p),

@@ -19,7 +19,7 @@
 #include <stdlib.h>
 #include <string.h>
 
-enum { MODE_REF64 = 0, MODE_REF32 = 1, MODE_FAST32 = 2 };
+enum { MODE_REF64 = 0, MODE_REF32 = 1, MODE_FAST32 = 2, MODE_SUM32 = 3 };
 
 static int lowbit(int r) { return r & -r; }
 
@@ -121,10 +121,15 @@ static void* run_job_ordered(void* p) {
         for (size_t i = 0; i < m; ++i) y[i] = y[i] + x[i];
       }
     }
-    if (j->mode == MODE_FAST32)
+    if (j->mode == MODE_FAST32) {
       oracle_update_fast32(j->w[0][l] + lo, j->v[l] + lo, j->grad[0][l] + lo, j->scale, (float)j->lr, j->mu, j->wd, m);
-    else
+    } else if (j->mode == MODE_SUM32) {  /* update off: the averaged tree-order sum */
+      float* w0 = j->w[0][l] + lo;
+      const float* g = j->grad[0][l] + lo;
+      for (size_t i = 0; i < m; ++i) w0[i] = j->scale * g[i];
+    } else {
       oracle_update_ref32(j->w[0][l] + lo, j->grad[0][l] + lo, j->lr, m);
+    }
     for (int r = 1; r < j->world; ++r) {
       int parent = r & (r - 1);
       memcpy(j->rx[r][l] + lo, j->w[parent][l] + lo, m * sizeof(float));

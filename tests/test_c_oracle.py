@@ -40,3 +40,18 @@ def test_c_exchange_port_matches_oracle(world, threads):
                                        weight_decay=5e-4)
         for r in range(world):
             assert ex.w[r][l].tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("mode", ["ref32", "sum32"])
+def test_c_exchange_port_other_modes(mode):
+    elems = [520, 25050, 5010]
+    world = 4
+    ex = CO.ExchangeWorld(world, elems)
+    grads = [[g.copy() for g in ex.grad[r]] for r in range(world)]
+    w0 = [a.copy() for a in ex.w[0]]
+    ex.iteration(mode, lr=0.05, threads=2)
+    for l in range(len(elems)):
+        kw = {"scale": 1.0 / world} if mode == "sum32" else {}
+        want = O.exchange_iteration([grads[r][l] for r in range(world)], w0[l], 0.05, mode, **kw)
+        for r in range(world):
+            assert ex.w[r][l].tobytes() == np.asarray(want, np.float32).tobytes()
