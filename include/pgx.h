@@ -201,8 +201,10 @@ enum pgx_variant {
   PGX_VARIANT_TWOSHOT_CEP = 5,/* reduce-scatter by the copy engines, then the SM owner
                                  kernel (fold + update + all-gather peer stores) on a
                                  capped grid: no per-part copy/event chain            */
-  PGX_VARIANT_ONESHOT_LL = 6  /* small fp32 layers, fence-free: ONESHOT with every value
+  PGX_VARIANT_ONESHOT_LL = 6,  /* small fp32 layers, fence-free: ONESHOT with every value
                                  carried as an 8-byte {value, epoch} word (2x bytes)  */
+  PGX_VARIANT_ONESHOT_L128 = 7 /* fp32 ONESHOT over 128-byte lines: 30 values + an 8-byte
+                                 epoch flag per line, fence-free (128/120 bytes)      */
 };
 
 typedef struct pgx_xchg_config {

@@ -28,6 +28,7 @@ MODE_REF64, MODE_REF32, MODE_FAST32, MODE_SUM32 = 0, 1, 2, 3
 VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE, VARIANT_NVLS, VARIANT_ONESHOT = 0, 1, 2, 3, 4
 VARIANT_TWOSHOT_CEP = 5
 VARIANT_ONESHOT_LL = 6
+VARIANT_ONESHOT_L128 = 7
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p

@@ -670,6 +670,115 @@ __global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_oneshot_ll(XArgs a
   retire(a.queue);
 }
 
+// ============================================================== ONESHOT_L128
+// ONESHOT over 128-byte lines: 30 fp32 values + an 8-byte {epoch, epoch} flag per line,
+// written by 8 lanes of a warp with one 16-byte volatile store each (one line = one
+// NVLink write, profiles/r4l: 25 M lines, none observed torn); the receiver polls the flag
+// word of each line (lane 7), then uses the line.  No fence, 128/120 bytes on the wire
+// (LL: 2x).  Items: C push chunks of lines, then C fold chunks (push-first claims).
+constexpr int kL128Vals = 30;
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_oneshot_l128(XArgs a) {
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  __shared__ uint32_t s_item;
+  const int me = a.rank;
+  const int lane = threadIdx.x & 31, q = lane >> 3, k = lane & 7;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint64_t lines = (a.S + kL128Vals - 1) / kL128Vals;
+  auto slot = [&](int r, int s) {  // rank r's slot [parity][s]: `lines` 128-byte lines
+    return static_cast<uint8_t*>(a.rx[r]) + (uint64_t)(parity * N + s) * a.sl * 4;
+  };
+  const int nv = k < 7 ? 4 : 2;  // values carried by this lane
+  while (true) {
+    uint32_t it = claim(a.queue, &s_item) + a.item_begin;
+    if (it >= a.item_end) break;
+    const bool push = it < a.push_items;
+    const uint32_t c = push ? it : it - a.push_items;
+    const uint64_t l_lo = (uint64_t)c * a.CH, l_hi = min(l_lo + a.CH, lines);  // CH = lines per chunk
+    bool failed = false;
+    for (uint64_t l0 = l_lo + (uint64_t)warp * 4; l0 < l_hi && !failed; l0 += (uint64_t)nwarps * 4) {
+      const uint64_t line = l0 + q;
+      const bool have = line < l_hi;
+      const uint64_t e0 = line * kL128Vals + 4 * k;
+      if (push) {
+        if (N == 1) break;
+        uint32_t w4[4] = {0u, 0u, epoch, epoch};
+        if (have)
+          for (int i = 0; i < nv; ++i)
+            if (e0 + i < a.S) w4[i] = __float_as_uint(grad_elem<float>(a.g, e0 + i));
+        if (have) {
+#pragma unroll
+          for (int d = 1; d < N; ++d) {
+            uint8_t* p = slot((me + d) % N, me) + line * 128 + 16 * k;
+            asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w4[0]), "r"(w4[1]),
+                         "r"(w4[2]), "r"(w4[3])
+                         : "memory");
+          }
+        }
+      } else {
+        float vals[N][4];
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          if (s == me) {
+            for (int i = 0; i < 4; ++i)
+              vals[s][i] = (have && i < nv && e0 + i < a.S) ? grad_elem<float>(a.g, e0 + i) : 0.f;
+            continue;
+          }
+          const uint8_t* p = slot(me, s) + line * 128 + 16 * k;
+          uint64_t t0 = 0;
+          for (uint32_t spins = 0;; ++spins) {
+            uint32_t x0 = 0, x1 = 0, x2 = 0, x3 = 0;
+            if (have)
+              asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                           : "l"(p)
+                           : "memory");
+            const unsigned ok = __ballot_sync(0xffffffffu, k == 7 && have && x2 == epoch && x3 == epoch);
+            const bool mine_ok = !have || ((ok >> (q * 8 + 7)) & 1u);
+            vals[s][0] = __uint_as_float(x0);
+            vals[s][1] = __uint_as_float(x1);
+            vals[s][2] = __uint_as_float(x2);
+            vals[s][3] = __uint_as_float(x3);
+            if (__all_sync(0xffffffffu, mine_ok)) break;
+            if (spins > 1024) __nanosleep(32);
+            if ((spins & 1023) == 1023) {  // warp-uniform give-up decision (lane 0 decides)
+              int stop = 0;
+              if (lane == 0) {
+                if (!t0) t0 = globaltimer_ns();
+                stop = (a.st.word && *(volatile uint32_t*)a.st.word) ||
+                       (a.st.timeout_ns && globaltimer_ns() - t0 > a.st.timeout_ns);
+                if (stop && a.st.word) atomicCAS(a.st.word, 0u, (uint32_t)PGX_E_TIMEOUT);
+              }
+              if (__shfl_sync(0xffffffffu, stop, 0)) {
+                failed = true;
+                break;
+              }
+            }
+          }
+          if (failed) break;
+        }
+        if (failed || !have) continue;
+        const bool fast = a.mode == PGX_MODE_FAST32;
+        float* wp = static_cast<float*>(a.model[me]);
+        for (int i = 0; i < nv; ++i) {
+          const uint64_t e = e0 + i;
+          if (e >= a.S) break;
+          float col[N];
+#pragma unroll
+          for (int s = 0; s < N; ++s) col[s] = vals[s][i];
+          float v = fast ? a.v[e] : 0.f;
+          const float w = a.mode == PGX_MODE_SUM32 ? 0.f : wp[e];
+          wp[e] = apply_update<float>(w, tree_sum<N>(col, AddF32{}), v, a);
+          if (fast) a.v[e] = v;
+        }
+      }
+    }
+  }
+  retire(a.queue);
+}
+
 // ============================================================== TREE (paper)
 // Up: chunk c: acc = own + child_0 + child_1 + ... (children ascending, each the
 // child's subtree sum), then to the parent's rx slot, or on rank 0 the update
@@ -1226,6 +1335,28 @@ int oneshot_ll_grid(int want, int dev) {
   return std::max(1, std::min(want, cap[dev]));
 }
 
+template <int N>
+int oneshot_l128_grid(int want, int dev) {
+  static int cap[PGX_MAX_RANKS] = {};
+  if (!cap[dev]) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_oneshot_l128<N>, kThreads, 0);
+    cap[dev] = std::max(1, per_sm) * sm_count(dev);
+  }
+  return std::max(1, std::min(want, cap[dev]));
+}
+
+void launch_oneshot_l128(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n)                                                                \
+  case n:                                                                          \
+    k_oneshot_l128<n><<<oneshot_l128_grid<n>(want, dev), kThreads, 0, s>>>(a);   \
+    break;
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
 void launch_oneshot_ll(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
   switch (N) {
 #define PGX_CASE(n)                                                            \
@@ -1713,7 +1844,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     const bool ch_given = cfg->layer_chunk_elems && cfg->layer_chunk_elems[l];
     uint64_t CH = ch_given ? cfg->layer_chunk_elems[l] : cfg->chunk_elems;
     if (!ch_given && N > 1 && P.variant != PGX_VARIANT_TWOSHOT_CE && P.variant != PGX_VARIANT_ONESHOT &&
-        P.variant != PGX_VARIANT_ONESHOT_LL &&
+        P.variant != PGX_VARIANT_ONESHOT_LL && P.variant != PGX_VARIANT_ONESHOT_L128 &&
         !(P.variant == PGX_VARIANT_TREE && !x->auto_chunk_tree) && !(P.variant == PGX_VARIANT_NVLS && !x->auto_chunk_nvls)) {
       // big shards: chunks of up to 64 K elements (~128 per shard) amortise the system fence
       // that ends every chunk; chunk_elems stays the minimum (profiles/r3e, r3n)
@@ -1777,6 +1908,29 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0)) * own * x->esz +
                     (P.S - own) * x->esz;
 
+    } else if (P.variant == PGX_VARIANT_ONESHOT_L128) {
+      if (x->esz != 4) {
+        delete x;
+        return fail(PGX_E_CONFIG, "layer %d: ONESHOT_L128 carries fp32 values (not ref64)", l);
+      }
+      const uint64_t lines = (P.S + kL128Vals - 1) / kL128Vals;
+      P.sl = align_up(lines * 32, kAlignElems);  // slot: `lines` 128-byte lines (in 4-byte units)
+      // chunk = lines per item: ~one item per SM per phase, at least 32 lines (4 per warp)
+      CH = std::max<uint64_t>(32, (lines + sms - 1) / sms);
+      if (ch_given) CH = std::max<uint64_t>(1, cfg->layer_chunk_elems[l] / kL128Vals);
+      P.CH = CH;
+      P.C = (uint32_t)((lines + CH - 1) / CH);
+      P.K = N;
+      P.rx_off = rxoff;
+      rxoff = align_up(rxoff + 2 * (uint64_t)N * P.sl, kAlignElems);
+      P.rxflag_off = rxfoff;  // no flags: the epoch rides in every line
+      P.push_items = P.C;
+      P.items = 2 * P.C;
+      P.expected = 0;
+      P.grid = (int)std::min<uint64_t>(P.items, cap);
+      P.nvlink_bytes = (uint64_t)(N - 1) * lines * 128;
+      P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0)) * P.S * x->esz +
+                    (uint64_t)(N - 1) * lines * 128;
     } else if (P.variant == PGX_VARIANT_ONESHOT_LL) {
       if (x->esz != 4) {
         delete x;
@@ -2001,13 +2155,17 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
   int prev;
   cudaGetDevice(&prev);
   if (prev != x->dev) cudaSetDevice(x->dev);
-  if (P.variant == PGX_VARIANT_ONESHOT_LL) {
+  if (P.variant == PGX_VARIANT_ONESHOT_LL || P.variant == PGX_VARIANT_ONESHOT_L128) {
     xrecord(x->ready[l], s);
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
     if (a.item_end > a.item_begin) {
       ++x->launches;
-      launch_oneshot_ll(x->world, (int)std::min<uint32_t>(a.item_end - a.item_begin, (uint32_t)P.grid), x->dev, s, a);
+      const int want = (int)std::min<uint32_t>(a.item_end - a.item_begin, (uint32_t)P.grid);
+      if (P.variant == PGX_VARIANT_ONESHOT_LL)
+        launch_oneshot_ll(x->world, want, x->dev, s, a);
+      else
+        launch_oneshot_l128(x->world, want, x->dev, s, a);
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = xrecord(x->done[l], s);

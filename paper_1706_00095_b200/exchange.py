@@ -25,7 +25,7 @@ from .errors import ConfigError, ShapeError
 
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
             "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP,
-            "oneshot_ll": _lib.VARIANT_ONESHOT_LL}
+            "oneshot_ll": _lib.VARIANT_ONESHOT_LL, "oneshot_l128": _lib.VARIANT_ONESHOT_L128}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 

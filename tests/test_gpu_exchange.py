@@ -35,7 +35,7 @@ def stepped_layer(xs, trs, l, k, pieces_by_rank):
 
     N = len(xs)
     sync = torch.cuda.synchronize
-    if xs[0].variants[l] in ("twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll"):
+    if xs[0].variants[l] in ("twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128"):
         for r in range(N):
             xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
         sync()
@@ -63,11 +63,12 @@ def split_pieces(g, cut):
 
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll"])
+@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
+                                     "oneshot_l128"])
 @pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64", "sum32"])
 def test_exchange_matches_oracle(cuda, N, variant, mode):
-    if variant == "oneshot_ll" and mode == "ref64":
-        pytest.skip("the LL one-shot carries fp32 values")
+    if variant in ("oneshot_ll", "oneshot_l128") and mode == "ref64":
+        pytest.skip("the LL one-shots carry fp32 values")
     elems = LENET if N in (2, 8) else CIFAR
     iters = 3
     dt = np.float64 if mode == "ref64" else np.float32
@@ -223,7 +224,8 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     world.close()
 
 
-@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll"])
+@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
+                                     "oneshot_l128"])
 def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
     """Layers smaller than one vector per rank (empty owner shards), ragged tails and a
     piece boundary inside a vector, 8 ranks stepped on one GPU, ref32 bit-exact."""

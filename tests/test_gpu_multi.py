@@ -108,7 +108,7 @@ def _ngpu():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll")
+@pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128")
                                           for m in ("ref32", "fast32")]
                          + [("nvls", "fast32")])
 def test_concurrent_exchange_matches_oracle(variant, mode):
@@ -322,7 +322,7 @@ def _fault_worker(rank, world, port, variant, q):
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot_ll"])
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot_ll", "oneshot_l128"])
 def test_dead_peer_surfaces_as_transport_error(variant):
     out = _spawn(_fault_worker, 2, variant)
     assert out[0][1].startswith("TransportError"), out
@@ -429,7 +429,7 @@ def _graph_worker(rank, world, port, variant, gate, use_graph, q):
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("variant,gate", [("auto", "layer"), ("auto", "model"), ("twoshot", "layer"),
                                           ("twoshot_ce", "layer"), ("twoshot_cep", "model"), ("tree", "layer"),
-                                          ("oneshot", "layer"), ("oneshot_ll", "model")])
+                                          ("oneshot", "layer"), ("oneshot_ll", "model"), ("oneshot_l128", "layer")])
 def test_graph_replay_multi_gpu_matches_oracle(variant, gate):
     out = _spawn(_graph_worker, _ngpu(), variant, gate, True)
     for rank, bad, status in out:
