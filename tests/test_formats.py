@@ -125,3 +125,31 @@ def test_timeline_csv_roundtrip_sorted(tmp_path):
     write_timeline_csv(evs, p)
     back = read_timeline_csv(p)
     assert back == sorted(evs, key=lambda e: (e.rank, e.t_start_ns, e.t_end_ns))
+
+
+def test_native_parse_property_against_oracle():
+    """Random PSGD1 blobs (oracle-made) and every truncation of a small one: the native
+    framing check accepts / rejects exactly like the oracle restatement, same messages."""
+    from paper_1706_00095_b200.checkpoint import image_bytes, parse
+    from paper_1706_00095_b200.errors import FormatError
+
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        sizes = [int(s) for s in rng.integers(0, 40, size=int(rng.integers(1, 6)))]
+        blob = O.ckpt_serialize([rng.standard_normal(s) for s in sizes])
+        assert parse(blob) == sizes
+        assert image_bytes(sizes) == len(blob)
+    blob = O.ckpt_serialize([np.arange(3.0), np.arange(2.0)])
+    for cut in range(len(blob)):
+        part = blob[:cut]
+        try:
+            O.ckpt_load(part)
+            want = None
+        except O.CheckpointFormatError as exc:
+            want = str(exc)
+        try:
+            parse(part)
+            got = None
+        except FormatError as exc:
+            got = str(exc)
+        assert got == want, cut
