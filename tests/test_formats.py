@@ -153,3 +153,23 @@ def test_native_parse_property_against_oracle():
         except FormatError as exc:
             got = str(exc)
         assert got == want, cut
+
+
+def test_timeline_overlap_property_against_oracle():
+    """Random event sets: the product's RunMetrics equal the oracle restatement exactly."""
+    from paper_1706_00095_b200.timeline import EVENT_KINDS, TimelineEvent, compute_overlap
+
+    kinds = sorted(EVENT_KINDS)
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        evs = []
+        for _ in range(int(rng.integers(0, 30))):
+            t0 = int(rng.integers(0, 5000))
+            evs.append((int(rng.integers(0, 4)), int(rng.integers(0, 3)), int(rng.integers(-1, 6)),
+                        kinds[int(rng.integers(0, len(kinds)))], t0, t0 + int(rng.integers(0, 2000))))
+        got = compute_overlap([TimelineEvent(*e) for e in evs])
+        want = O.overlap_metrics(evs)
+        assert got.overlap_ratio == want["overlap_ratio"]
+        assert got.iterations_per_second == want["iterations_per_second"]
+        assert got.wall_clock_ns == want["wall_clock_ns"]
+        assert got.per_rank_overlap == want["per_rank_overlap"]
