@@ -49,13 +49,14 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
-    p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "twoshot_cep", "nvls", "oneshot", "auto", "nccl_bulk", "ddp"],
+    p.add_argument("--variant", default="auto", choices=["twoshot", "tree", "twoshot_ce", "twoshot_cep", "twoshot_bulk", "nvls", "oneshot", "auto", "nccl_bulk",
+                            "ddp"],
                    help="nccl_bulk / ddp are comparison rows (NCCL on the path), not the product")
     p.add_argument("--chunk-elems", type=int, default=16384)
     p.add_argument("--gate", default="auto", choices=["auto", "layer", "model"],
                    help="per-layer forward gates, or one whole-model gate per step (auto: model if > 16 layers)")
     p.add_argument("--max-ctas", type=int, default=0)
-    p.add_argument("--large", choices=("ce", "cep", "sm"), default="ce",
+    p.add_argument("--large", choices=("ce", "cep", "sm", "bulk"), default="ce",
                    help="auto policy for layers >= 1M elements: copy-engine or SM two-shot")
     p.add_argument("--large-ctas", type=int, default=0, help="CTA cap of the large layers' launches (0 = auto)")
     p.add_argument("--large-chunk-elems", type=int, default=0, help="chunk of the large layers (0 = --chunk-elems)")
@@ -575,6 +576,7 @@ def pgx_arm(args):
     avg = statistics.median(durs) if durs else None  # median: one replay can catch a host hiccup
     kname = {"twoshot": "k_twoshot", "twoshot_ce": "k_owner_local + copy-engine transfers",
              "twoshot_cep": "k_twoshot owner items + copy-engine reduce-scatter",
+             "twoshot_bulk": "k_twoshot_bulk (TMA bulk copies, capped grid)",
              "tree": "k_tree_up/k_tree_down", "nvls": "k_nvls (multimem)",
              "oneshot": "k_oneshot"}[xchg.variants[L_DOM]]
     what = "%s, layer %d (%d params): fold + fused momentum update%s" % (

@@ -20,7 +20,7 @@
 extern "C" {
 #endif
 
-#define PGX_ABI_VERSION 2
+#define PGX_ABI_VERSION 3
 #define PGX_IPC_HANDLE_BYTES 64
 #define PGX_CONTROL_SEGMENT 15 /* transport/base.py:21 */
 #define PGX_MAX_RANKS 8
@@ -203,8 +203,23 @@ enum pgx_variant {
                                  capped grid: no per-part copy/event chain            */
   PGX_VARIANT_ONESHOT_LL = 6,  /* small fp32 layers, fence-free: ONESHOT with every value
                                  carried as an 8-byte {value, epoch} word (2x bytes)  */
-  PGX_VARIANT_ONESHOT_L128 = 7 /* fp32 ONESHOT over 128-byte lines: 30 values + an 8-byte
-                                 epoch flag per line, fence-free (128/120 bytes)      */
+  PGX_VARIANT_ONESHOT_L128 = 7,/* fp32 ONESHOT over 128-byte lines: 30 values + an 8-byte
+                                 epoch flag per line, fence-free (128/120 bytes); needs
+                                 PGX_XF_ALLOW_L128 (probed, not architecturally promised) */
+  PGX_VARIANT_TWOSHOT_BULK = 8 /* TWOSHOT with every NVLink byte moved by TMA bulk copies
+                                 (cp.async.bulk through a shared-memory ring, one thread
+                                 per CTA) on a capped grid, one system fence + flag per
+                                 ~1 MB slab: the large-layer variant                     */
+};
+
+/* pgx_xchg_config.flags (ABI 3: these were process-environment knobs before) */
+enum pgx_xchg_flag {
+  PGX_XF_CE_RS_PARTS = 1,          /* TWOSHOT_CE: part-major push with per-part signals     */
+  PGX_XF_TMA = 2,                  /* TWOSHOT: push + all-gather as TMA bulk copies          */
+  PGX_XF_ONESHOT_SMALL_CHUNKS = 4, /* ONESHOT: ~one chunk per SM (measured slower, r3v)      */
+  PGX_XF_AUTO_CHUNK_TREE = 8,      /* TREE: size-scaled chunks (measured slower, r3r)        */
+  PGX_XF_NO_AUTO_CHUNK_NVLS = 16,  /* NVLS: keep chunk_elems instead of size-scaled chunks   */
+  PGX_XF_ALLOW_L128 = 32           /* permit ONESHOT_L128 layers (sm_100 only)               */
 };
 
 typedef struct pgx_xchg_config {
@@ -222,6 +237,10 @@ typedef struct pgx_xchg_config {
   int max_ctas;                  /* CTAs per exchange launch (0 = auto) */
   const uint64_t* layer_chunk_elems; /* optional per-layer chunk_elems (NULL or 0 = chunk_elems) */
   const int* layer_max_ctas;     /* optional per-layer CTA cap (NULL or 0 = max_ctas) */
+  /* ABI 3 (0 = the default everywhere) */
+  int ce_parts;                  /* TWOSHOT_CE owner pipelining depth 1..8 (0 = 4)       */
+  int ce_rs_streams;             /* TWOSHOT_CE reduce-scatter copy streams 1..2 (0 = 1)  */
+  uint32_t flags;                /* pgx_xchg_flag bits                                    */
 } pgx_xchg_config;
 
 int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out);
@@ -287,6 +306,9 @@ int pgx_xchg_layer_bytes(pgx_xchg* x, int layer, uint64_t* nvlink_out_bytes,
 /* The plan a layer runs with: effective chunk elements (notification granularity) and
  * CTAs of its exchange kernel launch. */
 int pgx_xchg_layer_plan(pgx_xchg* x, int layer, uint64_t* chunk_elems_out, int* ctas_out);
+/* TWOSHOT_CE: how many pipelined parts this rank's owner shard of `layer` is split into
+ * (1 for every other variant). */
+int pgx_xchg_layer_parts(pgx_xchg* x, int layer, int* parts_out);
 /* Debug timeline: when `device_buffer` (u64 [items][4]) is non-NULL, instrumented kernels
  * (ONESHOT) stamp each work item's claim / mid / end globaltimer ns and SM id into it.
  * NULL turns it off (the default: one predicated-off branch per item). */

@@ -29,6 +29,8 @@ VARIANT_TREE, VARIANT_TWOSHOT, VARIANT_TWOSHOT_CE, VARIANT_NVLS, VARIANT_ONESHOT
 VARIANT_TWOSHOT_CEP = 5
 VARIANT_ONESHOT_LL = 6
 VARIANT_ONESHOT_L128 = 7
+VARIANT_TWOSHOT_BULK = 8
+XF_CE_RS_PARTS, XF_TMA, XF_ONESHOT_SMALL_CHUNKS, XF_AUTO_CHUNK_TREE, XF_NO_AUTO_CHUNK_NVLS, XF_ALLOW_L128 = 1, 2, 4, 8, 16, 32
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p
@@ -51,6 +53,9 @@ class XchgConfig(C.Structure):
         ("max_ctas", i32),
         ("layer_chunk_elems", P(u64)),
         ("layer_max_ctas", P(i32)),
+        ("ce_parts", i32),
+        ("ce_rs_streams", i32),
+        ("flags", u32),
     ]
 
 
@@ -104,6 +109,7 @@ SIGNATURES = {
     "pgx_xchg_nvls_bind": [vp],
     "pgx_xchg_layer_bytes": [vp, i32, P(u64), P(u64)],
     "pgx_xchg_layer_plan": [vp, i32, P(u64), P(i32)],
+    "pgx_xchg_layer_parts": [vp, i32, P(i32)],
     "pgx_xchg_set_trace": [vp, vp],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],

@@ -476,6 +476,205 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
   retire(a.queue);
 }
 
+// ============================================================== TWOSHOT_BULK
+// The two-shot schedule with every NVLink byte moved by the Tensor Memory Accelerator on
+// a capped grid (the large-layer variant): per CTA one thread streams a slab through a
+// shared-memory ring — cp.async.bulk global->smem (mbarrier complete_tx), smem->peer
+// global (bulk group), loads issued S-1 tiles ahead and ring slots recycled as soon as
+// the store has READ them (wait_group.read), so the bytes in flight on NVLink are not
+// bounded by the ring.  One system fence + release flag per slab (~1 MB), not per 64 KB
+// chunk (the per-chunk fence capped the register two-shot at ~7.5 GB/s per CTA).  Owner
+// slabs fold the N contributions in tree order (tree_sum<N>) tile by tile into the ring
+// and the elected thread bulk-stores each updated tile into every peer's weights.  16-24
+// CTAs saturate NVLink (tools/probe_push.cu: 689 GB/s push from 16 CTAs), so the layer
+// leaves the other SMs to the backward kernels it overlaps with.
+constexpr int kBulkThreads = 256;
+constexpr int kBulkStage = 32768;  // bytes per ring slot
+constexpr int kBulkStages = 4;
+constexpr size_t kBulkSmem = (size_t)kBulkStages * kBulkStage + kBulkStages * sizeof(uint64_t);
+constexpr int kBulkCtas = 24;      // default grid of a bulk layer
+
+__device__ __forceinline__ void tma_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_read_all_but(int k) {
+  // k is a compile-time ring depth minus one at every call site
+  if (k >= 3)
+    asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+  else if (k == 2)
+    asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+  else if (k == 1)
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  else
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+struct BulkSeg {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t bytes;  // multiple of 16, both ends 16-byte aligned
+};
+
+// Tile j of the concatenated segments.
+__device__ __forceinline__ uint32_t bulk_tile(const BulkSeg* s, int n, uint32_t j, const uint8_t** src, uint8_t** dst) {
+  for (int k = 0; k < n; ++k) {
+    const uint32_t t = (uint32_t)((s[k].bytes + kBulkStage - 1) / kBulkStage);
+    if (j < t) {
+      const uint64_t o = (uint64_t)j * kBulkStage;
+      *src = s[k].src + o;
+      *dst = s[k].dst + o;
+      return (uint32_t)min((uint64_t)kBulkStage, s[k].bytes - o);
+    }
+    j -= t;
+  }
+  return 0;
+}
+
+// One thread: copy the segments through the ring (loads S-1 tiles ahead).  `gload`
+// counts every load this CTA ever issued: load g uses slot g % S at mbarrier phase
+// (g / S) & 1.  Returns with stores possibly in flight (caller: wait_group 0).
+__device__ __forceinline__ void bulk_stream(const BulkSeg* segs, int nseg, uint8_t* ring, uint64_t* bars,
+                                            uint32_t& gload) {
+  constexpr int S = kBulkStages;
+  uint32_t n = 0;
+  for (int k = 0; k < nseg; ++k) n += (uint32_t)((segs[k].bytes + kBulkStage - 1) / kBulkStage);
+  auto load = [&](uint32_t j) {
+    const int s = (int)((gload + j) % S);
+    const uint8_t* src;
+    uint8_t* dst;
+    const uint32_t b = bulk_tile(segs, nseg, j, &src, &dst);
+    mbar_expect_tx(&bars[s], b);
+    tma_load(ring + (size_t)s * kBulkStage, src, b, &bars[s]);
+  };
+  const uint32_t pre = min(n, (uint32_t)(S - 1));
+  for (uint32_t j = 0; j < pre; ++j) load(j);
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t g = gload + j;
+    const int s = (int)(g % S);
+    mbar_wait(&bars[s], (g / S) & 1u);
+    const uint8_t* src;
+    uint8_t* dst;
+    const uint32_t b = bulk_tile(segs, nseg, j, &src, &dst);
+    tma_store(dst, ring + (size_t)s * kBulkStage, b);
+    tma_commit();
+    if (j + S - 1 < n) {
+      tma_wait_read_1();  // slot (j+S-1)%S was read by the store of tile j-1
+      load(j + S - 1);
+    }
+  }
+  gload += n;
+}
+
+template <int N, class T>
+__global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
+  constexpr int W = VecT<T>::W;
+  constexpr int S = kBulkStages;
+  constexpr uint64_t TE = kBulkStage / sizeof(T);  // elements per ring tile
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  extern __shared__ __align__(128) uint8_t ring[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)S * kBulkStage);
+  __shared__ uint32_t s_item;
+  __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < S; ++k) mbar_init(&bars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t gload = 0;  // thread 0's load counter (mbarrier phases)
+  const int me = a.rank;
+  while (true) {
+    const uint32_t it = claim(a.queue, &s_item) + a.item_begin;
+    if (it >= a.item_end) break;
+    if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // ring: generic <-> async
+    if (N > 1 && it < a.push_items) {
+      // ---- reduce-scatter: slab c of owner j's shard -> j's rx[parity][me]
+      constexpr int NP = N > 1 ? N - 1 : 1;
+      const uint32_t c = it / NP;
+      const int j = (me + 1 + (int)(it % NP)) % N;  // rotated: ranks start on different owners
+      const uint64_t lo = j * a.sl + (uint64_t)c * a.CH;
+      const uint64_t hi = min(min(lo + a.CH, (uint64_t)(j + 1) * a.sl), a.S);
+      if (lo >= hi) continue;
+      T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + (lo - j * a.sl));
+      BulkSeg segs[PGX_MAX_PIECES];
+      int nseg = 0;
+      uint64_t pb = 0;
+      for (int k = 0; k < a.g.n; ++k) {  // the slab may straddle gradient pieces (dW | db)
+        const uint64_t pe = a.g.end[k], ol = max(lo, pb), oh = min(hi, pe);
+        if (ol < oh) {
+          const T* src = static_cast<const T*>(a.g.p[k]) + (ol - pb);
+          T* d = dst + (ol - lo);
+          uint64_t head = 0, body = 0;
+          const uintptr_t sa = reinterpret_cast<uintptr_t>(src), da = reinterpret_cast<uintptr_t>(d);
+          if ((sa & 15) == (da & 15)) {  // co-aligned: scalar head, bulk body, scalar tail
+            head = min(oh - ol, (uint64_t)(((16 - (sa & 15)) & 15) / sizeof(T)));
+            body = ((oh - ol - head) * sizeof(T)) & ~uint64_t(15);
+          }
+          if (body) segs[nseg++] = {reinterpret_cast<const uint8_t*>(src + head), reinterpret_cast<uint8_t*>(d + head), body};
+          const uint64_t tail0 = head + body / sizeof(T);
+          for (uint64_t e = threadIdx.x; e < head; e += blockDim.x) d[e] = src[e];
+          for (uint64_t e = tail0 + threadIdx.x; e < oh - ol; e += blockDim.x) d[e] = src[e];
+        }
+        pb = pe;
+      }
+      if (threadIdx.x == 0 && nseg) bulk_stream(segs, nseg, ring, bars, gload);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma_wait_all();                                      // the slab's bulk writes are done
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        fence_acq_rel_sys();
+        st_release_sys(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
+      }
+    } else {
+      // ---- owner slab: fold N contributions in tree order, update, bulk all-gather
+      const uint32_t c = it - a.push_items;
+      const uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
+      const uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
+      if (lo >= hi) continue;
+      if (threadIdx.x < N - 1) {
+        const int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
+        s_flags[threadIdx.x] = a.rxflags[me] + (uint64_t)s * a.C + c;
+      }
+      __syncthreads();
+      cta_wait_flags(s_flags, N - 1, epoch, a.st);
+      const T* rxs = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
+      constexpr int U = (N <= 4 || sizeof(T) == 4) ? (N <= 4 ? 4 : 2) : 1;
+      uint32_t tile = 0;
+      for (uint64_t t0 = lo; t0 < hi; t0 += TE, ++tile) {
+        const uint64_t t1 = min(t0 + TE, hi);
+        T* stage = reinterpret_cast<T*>(ring + (size_t)(tile % S) * kBulkStage);
+        if (tile >= (uint32_t)S) {  // the slot's previous all-gather stores must have read it
+          if (threadIdx.x == 0) tma_wait_read_all_but(S - 1);
+          __syncthreads();
+        }
+        const uint64_t nvec = (t1 - t0 + W - 1) / W;
+        for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
+          owner_vectors<N, T, U, false>(a, rxs + (t0 - lo), t0, t1, q0, nvec, stage);
+        __syncthreads();
+        if (N > 1 && threadIdx.x == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+          const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
+          if (body) {
+            for (int d = 1; d < N; ++d)
+              tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, stage, (uint32_t)body);
+            tma_commit();
+          }
+          for (int d = 1; d < N; ++d) {  // ragged end of the layer (< 16 bytes)
+            uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
+            for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(stage)[b];
+          }
+        }
+      }
+      if (N > 1 && threadIdx.x == 0) {
+        tma_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        fence_acq_rel_sys();
+        for (int d = 1; d < N; ++d) red_release_sys_add(a.mflags[(me + d) % N] + a.layer, 1u);
+      }
+    }
+  }
+  if (threadIdx.x == 0) tma_wait_all();
+  retire(a.queue);
+}
+
 // Debug timeline (pgx_xchg_set_trace): item `it` -> [claim, mid, end, smid], thread 0 only.
 __device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slot) {
   if (a.trace && threadIdx.x == 0) {
@@ -1301,6 +1500,24 @@ void launch_twoshot(int N, bool tma, int want, int dev, cudaStream_t s, const XA
   }
 }
 
+template <class T>
+void launch_twoshot_bulk(int N, int grid, int dev, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n)                                                                                      \
+  case n: {                                                                                              \
+    static bool attr[64] = {};                                                                           \
+    if (!attr[dev & 63]) {                                                                               \
+      cudaFuncSetAttribute(k_twoshot_bulk<n, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem); \
+      attr[dev & 63] = true;                                                                             \
+    }                                                                                                    \
+    k_twoshot_bulk<n, T><<<grid, kBulkThreads, kBulkSmem, s>>>(a);                                       \
+    break;                                                                                               \
+  }
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
 template <int N, class T>
 int oneshot_grid(int want, int dev) {
   static int cap[PGX_MAX_RANKS] = {};
@@ -1813,6 +2030,21 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   if (cfg->chunk_elems < 4 || cfg->chunk_elems % 4) return fail(PGX_E_CONFIG, "chunk_elems must be a positive multiple of 4");
   if (cfg->mode < 0 || cfg->mode > 3) return fail(PGX_E_CONFIG, "unknown mode %d", cfg->mode);
   if (!(cfg->lr > 0)) return fail(PGX_E_CONFIG, "epsilon must be > 0, got %g", cfg->lr);
+  if (cfg->ce_parts < 0 || cfg->ce_parts > 8) return fail(PGX_E_CONFIG, "ce_parts must be 0 (default) or 1..8");
+  if (cfg->ce_rs_streams < 0 || cfg->ce_rs_streams > 2)
+    return fail(PGX_E_CONFIG, "ce_rs_streams must be 0 (default), 1 or 2");
+  for (int l = 0; l < cfg->num_layers; ++l) {
+    if (cfg->variant && cfg->variant[l] == PGX_VARIANT_ONESHOT_L128) {
+      // fence-free 128-byte lines rest on a probed (not promised) property of sm_100 NVLink
+      // writes: only on explicit request, only on that architecture
+      if (!(cfg->flags & PGX_XF_ALLOW_L128))
+        return fail(PGX_E_CONFIG, "layer %d: ONESHOT_L128 needs the PGX_XF_ALLOW_L128 opt-in flag", l);
+      int dev = 0, major = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+      if (major != 10) return fail(PGX_E_CONFIG, "ONESHOT_L128 was validated on sm_100 only (device is sm_%d x)", major);
+    }
+  }
   pgx_xchg* x = new pgx_xchg();
   x->w = w;
   x->cfg = *cfg;
@@ -1820,9 +2052,14 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   x->world = world_size(w);
   x->dev = world_device(w);
   x->esz = cfg->mode == PGX_MODE_REF64 ? 8 : 4;
-  if (const char* v = getenv("PGX_AUTO_CHUNK_TREE")) x->auto_chunk_tree = atoi(v) != 0;
-  if (const char* v = getenv("PGX_AUTO_CHUNK_NVLS")) x->auto_chunk_nvls = atoi(v) != 0;
-  if (const char* v = getenv("PGX_ONESHOT_SMALL_CHUNKS")) x->oneshot_small_chunks = atoi(v) != 0;
+  // former environment knobs, now part of the config (ABI 3); 0 = the measured defaults
+  x->auto_chunk_tree = (cfg->flags & PGX_XF_AUTO_CHUNK_TREE) != 0;
+  x->auto_chunk_nvls = (cfg->flags & PGX_XF_NO_AUTO_CHUNK_NVLS) == 0;
+  x->oneshot_small_chunks = (cfg->flags & PGX_XF_ONESHOT_SMALL_CHUNKS) != 0;
+  x->tma = (cfg->flags & PGX_XF_TMA) != 0;
+  x->ce_rs_parts = (cfg->flags & PGX_XF_CE_RS_PARTS) != 0;
+  if (cfg->ce_parts) x->ce_parts = cfg->ce_parts;
+  if (cfg->ce_rs_streams) x->ce_rs_streams = cfg->ce_rs_streams;
   x->seg_model = cfg->seg_base;
   x->seg_rx = cfg->seg_base + 1;
   const int N = x->world;
@@ -1844,6 +2081,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     const bool ch_given = cfg->layer_chunk_elems && cfg->layer_chunk_elems[l];
     uint64_t CH = ch_given ? cfg->layer_chunk_elems[l] : cfg->chunk_elems;
     if (!ch_given && N > 1 && P.variant != PGX_VARIANT_TWOSHOT_CE && P.variant != PGX_VARIANT_ONESHOT &&
+        P.variant != PGX_VARIANT_TWOSHOT_BULK &&
         P.variant != PGX_VARIANT_ONESHOT_LL && P.variant != PGX_VARIANT_ONESHOT_L128 &&
         !(P.variant == PGX_VARIANT_TREE && !x->auto_chunk_tree) && !(P.variant == PGX_VARIANT_NVLS && !x->auto_chunk_nvls)) {
       // big shards: chunks of up to 64 K elements (~128 per shard) amortise the system fence
@@ -1861,6 +2099,15 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       delete x;
       return fail(PGX_E_CONFIG, "layer %d: chunk_elems must be a positive multiple of 4", l);
     }
+    if (!ch_given && P.variant == PGX_VARIANT_TWOSHOT_BULK) {
+      // slabs (one fence + flag each) of 64 K .. 256 K elements, >= ~one owner slab per CTA
+      const uint64_t shard = (P.S + N - 1) / N;
+      const int g = (cfg->layer_max_ctas && cfg->layer_max_ctas[l] > 0) ? cfg->layer_max_ctas[l]
+                    : cfg->max_ctas > 0 ? cfg->max_ctas : kBulkCtas;
+      uint64_t c = (shard + g - 1) / g;
+      c = std::max<uint64_t>(65536, std::min<uint64_t>(262144, c));
+      CH = align_up(c, 8192);  // whole ring tiles (32 KB of fp32)
+    }
     P.CH = CH;
     // per-layer CTA cap (large layers: fewer CTAs with bigger chunks leave SMs to the backward)
     const bool lcapped = cfg->layer_max_ctas && cfg->layer_max_ctas[l] > 0;
@@ -1870,6 +2117,10 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       cap = std::min(cap, kCepCtas);
       capped = true;
     }
+    if (P.variant == PGX_VARIANT_TWOSHOT_BULK && !capped) {  // 16-24 TMA CTAs saturate NVLink (r3d)
+      cap = kBulkCtas;
+      capped = true;
+    }
     P.model_off = moff;
     moff = align_up(moff + P.S, kAlignElems);
     if (P.variant == PGX_VARIANT_NVLS && (cfg->mode != PGX_MODE_FAST32 || N < 2)) {
@@ -1877,7 +2128,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       return fail(PGX_E_CONFIG, "NVLS layers need fast32 and at least 2 ranks");
     }
     if (P.variant == PGX_VARIANT_TWOSHOT || P.variant == PGX_VARIANT_TWOSHOT_CE || P.variant == PGX_VARIANT_NVLS ||
-        P.variant == PGX_VARIANT_TWOSHOT_CEP) {
+        P.variant == PGX_VARIANT_TWOSHOT_CEP || P.variant == PGX_VARIANT_TWOSHOT_BULK) {
       P.sl = align_up((P.S + N - 1) / N, 4);
       P.C = (uint32_t)((P.sl + CH - 1) / CH);
       P.K = N;
@@ -2026,10 +2277,6 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_own, cudaStreamNonBlocking, hi_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_ag, cudaStreamNonBlocking, hi_prio);
     if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&x->ce_rs2, cudaStreamNonBlocking, hi_prio);
-    if (const char* v = getenv("PGX_CE_PARTS")) x->ce_parts = std::max(1, std::min(8, atoi(v)));
-    if (const char* v = getenv("PGX_CE_RS_STREAMS")) x->ce_rs_streams = std::max(1, std::min(2, atoi(v)));
-    if (const char* v = getenv("PGX_CE_RS_PARTS")) x->ce_rs_parts = atoi(v) != 0;
-    if (const char* v = getenv("PGX_TMA")) x->tma = atoi(v) != 0;
     x->done.resize(cfg->num_layers);
     x->ready.resize(cfg->num_layers);
     x->rs_done.resize(cfg->num_layers);
@@ -2209,7 +2456,19 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     return rc;
   }
   xrecord(x->ready[l], s);
-  if (P.variant == PGX_VARIANT_TWOSHOT) {
+  if (P.variant == PGX_VARIANT_TWOSHOT_BULK) {
+    a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
+    a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
+    uint32_t n = a.item_end > a.item_begin ? a.item_end - a.item_begin : 0;
+    if (n) {
+      ++x->launches;
+      int grid = (int)std::min<uint32_t>(n, (uint32_t)P.grid);
+      if (x->esz == 8)
+        launch_twoshot_bulk<double>(x->world, grid, x->dev, s, a);
+      else
+        launch_twoshot_bulk<float>(x->world, grid, x->dev, s, a);
+    }
+  } else if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;
     uint32_t n = a.item_end > a.item_begin ? a.item_end - a.item_begin : 0;
@@ -2391,6 +2650,12 @@ int pgx_xchg_layer_bytes(pgx_xchg* x, int l, uint64_t* nvl, uint64_t* hbm) {
   if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
   if (nvl) *nvl = x->L[l].nvlink_bytes;
   if (hbm) *hbm = x->L[l].hbm_bytes;
+  return PGX_OK;
+}
+
+int pgx_xchg_layer_parts(pgx_xchg* x, int l, int* parts) {
+  if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
+  *parts = x->L[l].variant == PGX_VARIANT_TWOSHOT_CE ? ce_split(x, x->L[l], x->rank, 0, nullptr, nullptr) : 1;
   return PGX_OK;
 }
 

@@ -25,7 +25,11 @@ from .errors import ConfigError, ShapeError
 
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
             "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP,
-            "oneshot_ll": _lib.VARIANT_ONESHOT_LL, "oneshot_l128": _lib.VARIANT_ONESHOT_L128}
+            "oneshot_ll": _lib.VARIANT_ONESHOT_LL, "oneshot_l128": _lib.VARIANT_ONESHOT_L128,
+            "twoshot_bulk": _lib.VARIANT_TWOSHOT_BULK}
+FLAGS = {"ce_rs_parts": _lib.XF_CE_RS_PARTS, "tma": _lib.XF_TMA, "oneshot_small_chunks": _lib.XF_ONESHOT_SMALL_CHUNKS,
+         "auto_chunk_tree": _lib.XF_AUTO_CHUNK_TREE, "no_auto_chunk_nvls": _lib.XF_NO_AUTO_CHUNK_NVLS,
+         "allow_l128": _lib.XF_ALLOW_L128}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 
@@ -40,7 +44,8 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
     (profiles/r3v: 14–21 µs up to 256 KB at N=4, NCCL 17–23).  large="sm"
     keeps the SM two-shot for the large layers too (run with a CTA cap and big chunks,
     see DeviceExchange `large_ctas`); large="cep" moves the reduce-scatter by copy engine
-    and runs fold + update + all-gather as the SM owner kernel on a capped grid."""
+    and runs fold + update + all-gather as the SM owner kernel on a capped grid;
+    large="bulk" moves every byte with TMA bulk copies from a capped grid (TWOSHOT_BULK)."""
     if oneshot_below is None:  # one-shot moves (N-1)*S per GPU: the crossover shrinks with N
         oneshot_below = (1 << 20) // max(world, 1)  # N=4: 1 MB layers (profiles/r2b_sweep_n4)
     if world > 1 and elems < tree_below:
@@ -50,7 +55,7 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
     if world > 1 and elems < oneshot_below:
         return "oneshot"
     if world > 1 and elems >= ce_from:
-        return {"ce": "twoshot_ce", "cep": "twoshot_cep", "sm": "twoshot"}[large]
+        return {"ce": "twoshot_ce", "cep": "twoshot_cep", "sm": "twoshot", "bulk": "twoshot_bulk"}[large]
     return "twoshot"
 
 
@@ -60,13 +65,16 @@ class DeviceExchange:
                  momentum: float = 0.0, weight_decay: float = 0.0, seg_base: int = 16, max_ctas: int = 0,
                  tree_below: int = 0, low_priority_from: int | None = None, large: str = "ce",
                  large_from: int = 1 << 20, large_ctas: int = 0, large_chunk_elems: int = 0,
-                 layer_chunk_elems=None, layer_max_ctas=None):
+                 layer_chunk_elems=None, layer_max_ctas=None, ce_parts: int = 0, ce_rs_streams: int = 0,
+                 flags=()):
         """variant: one name, a per-layer list, or "auto" (choose_variant; `large` = "ce" or
         "sm" for layers of >= `large_from` elements).  Layers of >= `large_from` elements get
         `large_chunk_elems` / `large_ctas` (0 = the global chunk_elems / max_ctas): fewer CTAs
         with bigger chunks move the same bytes with far fewer per-chunk system fences
         (profiles/r3e), leaving SMs to the backward kernels.  layer_chunk_elems /
-        layer_max_ctas override per layer (0 = default)."""
+        layer_max_ctas override per layer (0 = default).  ce_parts / ce_rs_streams / flags
+        (names of FLAGS) are the library's tuning knobs (pgx_xchg_config, ABI 3); the
+        defaults are the measured choices."""
         if mode not in MODES:
             raise ConfigError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
         self.tr = transport
@@ -103,7 +111,8 @@ class DeviceExchange:
             num_layers=L, layer_elems=self._elems, variant=self._vars, mode=MODES[mode],
             chunk_elems=int(chunk_elems), lr=float(lr), scale=self.scale, momentum=float(momentum),
             weight_decay=float(weight_decay), seg_base=int(seg_base), max_ctas=int(max_ctas),
-            layer_chunk_elems=self._chunks, layer_max_ctas=self._ctas)
+            layer_chunk_elems=self._chunks, layer_max_ctas=self._ctas, ce_parts=int(ce_parts),
+            ce_rs_streams=int(ce_rs_streams), flags=self._flag_bits(flags))
         h = C.c_void_p()
         _lib.call("pgx_xchg_create", transport.handle, C.byref(cfg), C.byref(h))
         self.handle = h
@@ -142,6 +151,21 @@ class DeviceExchange:
                                      for _ in range(_lib.XCHG_STREAMS)]
         arr = (C.c_void_p * _lib.XCHG_STREAMS)(*[s.cuda_stream for s in self.internal_streams])
         _lib.call("pgx_xchg_set_streams", h, arr, _lib.XCHG_STREAMS)
+
+    @staticmethod
+    def _flag_bits(flags) -> int:
+        bits = 0
+        for f in flags:
+            if f not in FLAGS:
+                raise ConfigError(f"unknown exchange flag {f!r}; known: {sorted(FLAGS)}")
+            bits |= FLAGS[f]
+        return bits
+
+    def ce_parts(self, layer: int) -> int:
+        """Pipelined owner parts of this rank's shard (copy-engine layers; 1 otherwise)."""
+        n = C.c_int()
+        _lib.call("pgx_xchg_layer_parts", self.handle, layer, C.byref(n))
+        return n.value
 
     def _nvls_setup(self) -> None:
         """Collective: rank 0's multicast handle reaches every rank as a file descriptor over

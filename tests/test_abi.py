@@ -27,7 +27,7 @@ def test_every_header_symbol_is_exported_and_bound():
 
 def test_abi_version_and_error_channel():
     lib = _lib.lib()
-    assert lib.pgx_abi_version() == 2
+    assert lib.pgx_abi_version() == 3
     assert isinstance(_lib.last_error(), str)
 
 

@@ -24,18 +24,21 @@ def build(N, elems, mode, variant, chunk_elems=4096, **kw):
 
     world = LocalWorld(N, inline=False)
     trs = [world.transport(r) for r in range(N)]
+    if variant == "oneshot_l128":  # opt-in only (pgx.h PGX_XF_ALLOW_L128)
+        kw.setdefault("flags", ("allow_l128",))
     xs = [DeviceExchange(tr, elems, mode=mode, variant=variant, chunk_elems=chunk_elems, **kw) for tr in trs]
     for x in xs:
         x.connect()
     return world, trs, xs
 
 
-def stepped_layer(xs, trs, l, k, pieces_by_rank):
+def stepped_layer(xs, trs, l, k, pieces_by_rank, gate=True):
     from paper_1706_00095_b200 import _lib
 
     N = len(xs)
     sync = torch.cuda.synchronize
-    if xs[0].variants[l] in ("twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128"):
+    if xs[0].variants[l] in ("twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128",
+                            "twoshot_bulk"):
         for r in range(N):
             xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
         sync()
@@ -49,8 +52,9 @@ def stepped_layer(xs, trs, l, k, pieces_by_rank):
         for r in range(N):  # parents before children
             xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=_lib.PHASE_DOWN)
             sync()
-    for r in range(N):
-        xs[r].gate(l, k, stream=trs[r].stream)
+    if gate:
+        for r in range(N):
+            xs[r].gate(l, k, stream=trs[r].stream)
     sync()
     for tr in trs:
         assert tr.device_status() == 0
@@ -64,7 +68,7 @@ def split_pieces(g, cut):
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128"])
+                                     "oneshot_l128", "twoshot_bulk"])
 @pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64", "sum32"])
 def test_exchange_matches_oracle(cuda, N, variant, mode):
     if variant in ("oneshot_ll", "oneshot_l128") and mode == "ref64":
@@ -176,7 +180,7 @@ class _FixedGrad(torch.nn.Module):
         return (self.weight * self.c).sum() + (self.bias * self.d).sum()
 
 
-@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll"])
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "twoshot_bulk"])
 @pytest.mark.parametrize("gate", ["layer", "model"])
 def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     """A captured training step (device iteration counter) applies exactly the oracle update."""
@@ -187,7 +191,8 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     layers = [(m, [m.weight, m.bias])]
     world = LocalWorld(1, inline=False)
     tr = world.transport(0)
-    x = DeviceExchange(tr, [40007], mode="fast32", variant=variant, lr=0.05, momentum=0.9, weight_decay=1e-3)
+    x = DeviceExchange(tr, [40007], mode="fast32", variant=variant, lr=0.05, momentum=0.9, weight_decay=1e-3,
+                       flags=(("allow_l128",) if variant == "oneshot_l128" else ()))
     x.connect()
     w = torch.cat([m.weight.detach(), m.bias.detach()]).cpu().numpy()
     g = torch.cat([m.c, m.d]).cpu().numpy()
@@ -225,7 +230,7 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128"])
+                                     "oneshot_l128", "twoshot_bulk"])
 def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
     """Layers smaller than one vector per rank (empty owner shards), ragged tails and a
     piece boundary inside a vector, 8 ranks stepped on one GPU, ref32 bit-exact."""

@@ -62,9 +62,11 @@ def main():
     xs = {}
     seg = 16
     for v in variants:
-        if v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "nvls", "oneshot", "oneshot_ll", "oneshot_l128"):
+        if v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "nvls", "oneshot", "oneshot_ll", "oneshot_l128",
+                 "twoshot_bulk"):
             xs[v] = DeviceExchange(tr, elems, mode=args.mode, variant=v, chunk_elems=args.chunk, lr=0.01,
-                                   momentum=0.9, weight_decay=5e-4, seg_base=seg, max_ctas=args.ctas)
+                                   momentum=0.9, weight_decay=5e-4, seg_base=seg, max_ctas=args.ctas,
+                                   flags=("allow_l128",) if v == "oneshot_l128" else ())
             seg += 2
     tr.barrier()
     for x in xs.values():
