@@ -45,7 +45,7 @@ NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--workload", default="alexnet", choices=["alexnet", "googlenet"])
+    p.add_argument("--workload", default="alexnet", choices=["alexnet", "googlenet", "lenet", "cifar10_quick"])
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="pgx", choices=["pgx", "reference"])
@@ -80,61 +80,147 @@ def cpu_info():
     return model, len(os.sched_getaffinity(0))
 
 
-# ------------------------------------------------------------------ CPU port
-CPU_SAMPLE_IMAGES = 8
+# ------------------------------------------------------------------ CPU side
+# The reference is CPU code: its exchange engine is pipesgd's PipelinedRank over InprocWorld
+# (pipelined.py:44-80), which bench.py runs from baseline/_ref (the reference package,
+# installed unmodified; it travels to the GPU box) and restates in C (oracle/pgx_oracle.c,
+# threaded, the "port").  The networks' forward/backward is not part of the reference; the
+# CPU training step below runs it in PyTorch-CPU on the FULL batch (no extrapolation).
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 
-def _cpu_fwd_bwd(model, x, y):
-    loss = model.loss(model(x), y)
-    loss.backward()
-    model.zero_grad(set_to_none=True)
-
-
-def cpu_step_timing(world: int, *, steps: int | None = None, seconds: float | None = None, warmup: int = 1,
-                    workload: str = "alexnet"):
-    """The same training step on the host CPU: AlexNet forward+backward in PyTorch-CPU
-    fp32 on a bounded sample of CPU_SAMPLE_IMAGES images (per-image cost scaled to the
-    256-image global batch), plus the reference's exchange data plane (tree fold, master
-    update, tree broadcast over `world` ranks) restated in C (oracle/pgx_oracle.c) on the
-    full AlexNet parameter set.  All host threads."""
+def _mk_batch(wl, n, seed=0):
     import torch
 
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(n, wl.get("channels", 3), wl["image"], wl["image"], generator=g)
+    y = torch.randint(0, wl.get("classes", 1000), (n,), generator=g)
+    return x, y
+
+
+def cpu_fwd_bwd_ms(net, x, y) -> float:
+    t0 = time.perf_counter()
+    loss = net.loss(net(x), y)
+    loss.backward()
+    net.zero_grad(set_to_none=True)
+    return (time.perf_counter() - t0) * 1e3
+
+
+def port_exchange(world: int, sizes, iters: int = 3, threads: int | None = None):
+    """(median ms, ExchangeWorld) of the C port of the reference's exchange iteration (tree
+    fold in the binomial order, fused update, broadcast) at `world` ranks on host threads."""
     from oracle import c_oracle as CO
+
+    threads = threads or cpu_info()[1]
+    ex = CO.ExchangeWorld(world, sizes, fast_fill=True)
+    ex.iteration("fast32", threads=threads)  # warm (page faults)
+    ts = []
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        ex.iteration("fast32", lr=0.01, mu=0.9, wd=5e-4, threads=threads)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return statistics.median(ts), ex
+
+
+def reference_engine_ms(world: int, sizes, iters: int = 2) -> dict:
+    """The reference's own exchange engine (pipesgd PipelinedRank.begin_iteration / run_turn /
+    finalize_iteration over InprocWorld, zero latency, f64 — pipelined.py:44-80) at the given
+    per-layer sizes (DenseLayerSpec(S-1, 1) so param_count = S).  Rank threads are
+    GIL-serialised and numpy is single-threaded: about one core.  Last iteration's time, max
+    over the rank threads."""
+    import threading
+
+    import numpy as np
+
+    if not os.path.isdir(os.path.join(REF_PATH, "pipesgd")):
+        return {"unavailable": f"reference package not installed at {REF_PATH}"}
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        from pipesgd.engine import PipelinedRank, TrainConfig
+        from pipesgd.net import DenseLayerSpec
+        from pipesgd.transport import InprocWorld
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"cannot import the reference: {exc!r}"}
+    cfg = TrainConfig(layer_dims=(2, 1), world_size=world, iterations=iters, batch_size=world,
+                      chunk_bytes=65536, finalize_timeout_s=600.0)
+    specs = [DenseLayerSpec(int(n) - 1, 1, "identity") for n in sizes]
+    cfg.specs = lambda: specs
+    w = InprocWorld(world)
+    try:
+        ranks = [PipelinedRank(cfg, None, w.transport(r)) for r in range(world)]
+        rng = np.random.default_rng(0)
+        grads = [rng.standard_normal(int(n)) * 1e-3 for n in sizes]  # values do not change the work
+        times = [[0.0] * iters for _ in range(world)]
+
+        def body(r):
+            rk = ranks[r]
+            for k in range(iters):
+                t0 = time.perf_counter()
+                rk.begin_iteration(k)
+                for l in reversed(range(len(sizes))):
+                    rk.run_turn(l, grads[l])
+                rk.finalize_iteration()
+                times[r][k] = time.perf_counter() - t0
+
+        ths = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+    finally:
+        w.close()
+    per_it = [max(times[r][k] for r in range(world)) * 1e3 for k in range(iters)]
+    return {"ms": per_it[-1], "iterations": iters, "all_ms": [round(t, 3) for t in per_it],
+            "engine": "pipesgd PipelinedRank over InprocWorld (baseline/_ref, f64, ~1 core)"}
+
+
+def cpu_step(world: int, wl_name: str, *, steps: int | None = None, seconds: float | None = None,
+             warmup: int = 1) -> dict:
+    """The training step on the host: the full global batch through PyTorch-CPU fp32 fwd+bwd
+    (all threads) plus one exchange iteration of the C port at `world` ranks, every counted
+    step measured (no sample scaling)."""
+    import torch
+
+    from workloads import WORKLOADS
 
     model_name, ncpu = cpu_info()
     torch.set_num_threads(ncpu)
-    from workloads import WORKLOADS
-
-    wl = WORKLOADS[workload]
+    wl = WORKLOADS[wl_name]
     net = wl["cls"]()
     gb = global_batch(wl, world)
     sizes = [sum(p.numel() for p in ps) for _, ps in net.layers()]
-    g = torch.Generator().manual_seed(0)
-    x = torch.randn(CPU_SAMPLE_IMAGES, 3, wl["image"], wl["image"], generator=g)
-    y = torch.randint(0, 1000, (CPU_SAMPLE_IMAGES,), generator=g)
-    ex = CO.ExchangeWorld(world, sizes)
+    x, y = _mk_batch(wl, gb)
+    ex_ms, ex = port_exchange(world, sizes, iters=1)
     for _ in range(warmup):
-        _cpu_fwd_bwd(net, x, y)
-        ex.iteration("fast32", threads=ncpu)
+        cpu_fwd_bwd_ms(net, x, y)
     fb, xc = [], []
     t_end = time.perf_counter() + (seconds or 1e9)
-    while (steps is None or len(fb) < steps) and time.perf_counter() < t_end:
+    while (steps is None or len(fb) < steps) and (time.perf_counter() < t_end or not fb):
+        fb.append(cpu_fwd_bwd_ms(net, x, y))
         t0 = time.perf_counter()
-        _cpu_fwd_bwd(net, x, y)
-        t1 = time.perf_counter()
         ex.iteration("fast32", lr=0.01, mu=0.9, wd=5e-4, threads=ncpu)
-        t2 = time.perf_counter()
-        fb.append((t1 - t0) * gb / CPU_SAMPLE_IMAGES)
-        xc.append(t2 - t1)
-    t_fb, t_x = statistics.median(fb), statistics.median(xc)
-    t = t_fb + t_x
-    return {"value": gb / t, "unit": "images/s", "cores": ncpu, "kind": "port",
-            "sample": f"{len(fb)} steps; each: {workload} fwd+bwd of {CPU_SAMPLE_IMAGES} images in PyTorch-CPU fp32 "
-                      f"scaled x{gb / CPU_SAMPLE_IMAGES:g} to the {gb}-image step, plus one full "
-                      f"exchange of the {sum(sizes):,} fp32 params at world {world} (C port of the reference's tree "
-                      f"fold + update + broadcast); cpu {model_name}",
-            "ms_per_step": t * 1e3, "ms_fwd_bwd": t_fb * 1e3, "ms_exchange": t_x * 1e3,
-            "exchange_only_images_per_s": gb / t_x}
+        xc.append((time.perf_counter() - t0) * 1e3)
+    tot = [a + b for a, b in zip(fb, xc)]
+    ms = sum(tot) / len(tot)
+    return {"value": gb / (ms / 1e3), "unit": "images/s", "cores": ncpu, "kind": "port",
+            "sample": f"{len(fb)} full steps; each: {wl_name} fwd+bwd of the whole {gb}-image batch in PyTorch-CPU "
+                      f"fp32 (not part of the reference, which has no conv nets) + one exchange iteration of the "
+                      f"{sum(sizes):,} fp32 params at world {world} by the C port of the reference's tree fold + "
+                      f"update + broadcast (oracle/pgx_oracle.c, {ncpu} threads); cpu {model_name}",
+            "ms_per_step": ms, "ms_fwd_bwd": statistics.median(fb), "ms_exchange": statistics.median(xc),
+            "exchange_only_images_per_s": gb / (statistics.median(xc) / 1e3), "steps_measured": len(fb)}
+
+
+def exchange_by_world(sizes, worlds=(2, 4, 8)) -> dict:
+    """CPU exchange per iteration at each world size: the C port and the reference's own
+    engine (BASELINE.md §2 measured 1.1 / 3.6 / 16.8 s for AlexNet)."""
+    out = {}
+    for w in worlds:
+        ms, ex = port_exchange(w, sizes, iters=3)
+        del ex
+        out[str(w)] = {"port_ms": ms, "port_threads": cpu_info()[1], "reference_engine": reference_engine_ms(w, sizes)}
+    return out
 
 
 def reference_arm(args):
@@ -142,13 +228,23 @@ def reference_arm(args):
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    r = cpu_step_timing(world, steps=args.steps, warmup=max(1, min(args.warmup, 2)), workload=args.workload)
-    line = {"metric": wl_of(args)["metric"], "value": r["value"], "unit": "images/s", "n_gpus": world, "steps": args.steps,
+    wl = wl_of(args)
+    sizes = [sum(p.numel() for p in ps) for _, ps in wl["cls"]().layers()]
+    r = cpu_step(world, args.workload, steps=args.steps, warmup=max(1, min(args.warmup, 2)))
+    ref = reference_engine_ms(world, sizes) if world > 1 or args.workload != "alexnet" else \
+        reference_engine_ms(1, sizes)
+    cfg = workload_config(world, args)
+    cfg.update({"fwd_bwd": "PyTorch-CPU fp32, full batch every step", "exchange": "C port of the reference's "
+                "exchange (tree fold + update + broadcast), all host threads", "step": "eager (CPU)"})
+    for k in ("chunk_elems", "large_layers", "gate"):
+        cfg.pop(k, None)
+    cb = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "ms_fwd_bwd", "ms_exchange",
+                            "exchange_only_images_per_s", "steps_measured")}
+    cb["reference_engine_exchange"] = ref
+    line = {"metric": wl["metric"], "value": r["value"], "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-            "scaling": wl_of(args)["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": workload_config(world, args),
-            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "ms_fwd_bwd",
-                                               "ms_exchange", "exchange_only_images_per_s")},
+            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": cfg, "cpu_baseline": cb,
             "e2e": {"value": r["value"], "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -156,15 +252,19 @@ def reference_arm(args):
 def workload_config(world, args):
     wl = wl_of(args)
     gb = global_batch(wl, world)
-    name = {"alexnet": "alexnet_b256_synthetic_227", "googlenet": "googlenet_b32pergpu_synthetic_224"}[args.workload]
+    name = {"alexnet": "alexnet_b256_synthetic_227", "googlenet": "googlenet_b32pergpu_synthetic_224",
+            "lenet": "lenet5_b64_synthetic_28", "cifar10_quick": "cifar10_quick_b100pergpu_synthetic_32"}[args.workload]
     model = {"alexnet": "AlexNet (BVLC, grouped conv, LRN)",
-             "googlenet": "GoogLeNet (BVLC, both aux heads, 64 param layers)"}[args.workload]
+             "googlenet": "GoogLeNet (BVLC, both aux heads, 64 param layers)",
+             "lenet": "LeNet-5 (Caffe lenet_train_test)", "cifar10_quick": "cifar10_quick (Caffe)"}[args.workload]
     h = wl["hyper"]
     return {"workload": name, "model": model,
-            "global_batch": gb, "per_gpu_batch": gb // world, "image": [3, wl["image"], wl["image"]],
+            "global_batch": gb, "per_gpu_batch": gb // world,
+            "image": [wl.get("channels", 3), wl["image"], wl["image"]],
             "parallelism": f"dp{world}", "exchange": args.variant, "update": f"fast32 momentum SGD lr {h['lr']} mu {h['momentum']} "
             f"wd {h['weight_decay']} scale 1/N", "fwd_bwd": "PyTorch cuDNN bf16 autocast, fp32 master weights/grads",
-            "l2": "working set > L2 (244 MB fp32 weights + 244 MB grads + activations per step)",
+            "l2": "working set > L2 (244 MB fp32 weights + 244 MB grads + activations per step)"
+                  if args.workload == "alexnet" else "per-step working set (weights, grads, activations)",
             "chunk_elems": args.chunk_elems, "large_layers": {"variant": args.large, "ctas": args.large_ctas,
                                                                "chunk_elems": args.large_chunk_elems},
             "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager"}
@@ -319,8 +419,9 @@ def pgx_arm(args):
     IMG = wl["image"]
     gb = B * world  # images per step, whole job
     g = torch.Generator().manual_seed(42 + rank)
-    host_x = torch.randint(0, 256, (B, 3, IMG, IMG), dtype=torch.uint8, generator=g).pin_memory()
-    host_y = torch.randint(0, 1000, (B,), dtype=torch.int64, generator=g).pin_memory()
+    CH_IN, NCLS = wl.get("channels", 3), wl.get("classes", 1000)
+    host_x = torch.randint(0, 256, (B, CH_IN, IMG, IMG), dtype=torch.uint8, generator=g).pin_memory()
+    host_y = torch.randint(0, NCLS, (B,), dtype=torch.int64, generator=g).pin_memory()
     dev_x, dev_y = host_x.to(dev), host_y.to(dev)
     loss_host = torch.zeros(max(args.steps, 1), dtype=torch.float32).pin_memory()
 
@@ -492,6 +593,7 @@ def pgx_arm(args):
 
     # ---- timeline: a few traced eager steps, reference CSV schema + overlap ----
     timeline = trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world)
+    timeline.update(pipelined_vs_barrier(bind, step, dev_x, dev_y, world))
 
     # ---- per-layer exchange in isolation (same launch, no concurrent backward, host enqueue
     # latency hidden behind a busy kernel so the events bracket device time): every rank,
@@ -524,6 +626,39 @@ def pgx_arm(args):
             ms_ = float(t.item())
         return ms_
 
+    # whole-model exchange alone (every layer in emission order, back to back, no backward):
+    # the exchange-only time per iteration, beside the CPU reference's (exchange_only below)
+    def whole_model(reps=10):
+        pieces = [[torch.randn_like(p) * 1e-3 for p in ps] for _, ps in model.layers()]
+        ts = []
+        for i in range(reps):
+            tr.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(xchg.stream):
+                torch.cuda._sleep(HOLD_CYCLES)
+            if world > 1:
+                tr.barrier_async(xchg.stream)
+            e0.record(xchg.stream)
+            for l in reversed(range(len(sizes))):
+                s_l = xchg.stream_for(l)
+                if s_l is not xchg.stream:
+                    s_l.wait_stream(xchg.stream)
+                xchg.launch(l, bind.k + i, pieces[l], stream=s_l)
+            for l in range(len(sizes)):
+                xchg.join(l, xchg.stream)
+            xchg.gate_all(bind.k + i, stream=xchg.stream)
+            e1.record(xchg.stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        bind.k += reps
+        ms_ = statistics.median(ts)
+        if world > 1:
+            t = torch.tensor([ms_])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_ = float(t.item())
+        return ms_
+
+    xchg_ms = whole_model()
     iso = [isolated(L_DOM)]
     by_layer = []
     if world > 1:
@@ -613,14 +748,33 @@ def pgx_arm(args):
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
             "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None, "timeline": timeline,
             "exchange_by_layer": by_layer or None, "exchange_by_layer_sm_twoshot": by_layer_sm or None}
+    # ---- exchange only: the whole model's exchange per iteration, GPU (device time, every layer
+    # back to back, no backward) vs the CPU reference at the same world size (rank 0 only) ----
+    xo = {"gpu_ms": xchg_ms, "world": world, "model_bytes_fp32": 4 * sum(sizes),
+          "gpu_measured": "all layers launched back to back in emission order + whole-model gate, device time, "
+                          "median of 10, max over ranks"}
+    if rank == 0 and not args.no_cpu_baseline:
+        port_ms, ex = port_exchange(world, sizes, iters=3)
+        del ex
+        xo.update({"cpu_port_ms": port_ms, "cpu_port_threads": cpu_info()[1],
+                   "port_over_gpu": port_ms / xchg_ms})
+        if world > 1 or args.workload != "alexnet":
+            ref = reference_engine_ms(world, sizes)
+            xo["cpu_reference_engine"] = ref
+            if "ms" in ref:
+                xo["reference_engine_over_gpu"] = ref["ms"] / xchg_ms
+    line["exchange_only"] = xo
     if args.per_gpu_batch:
         line["config"]["per_gpu_batch"] = B
         line["config"]["global_batch"] = gb
         line["config"]["diagnostic"] = "per-GPU batch overridden; not the headline configuration"
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_step_timing(world, seconds=args.cpu_seconds, workload=args.workload)
+        line["cpu_baseline"] = cpu_step(world, args.workload, seconds=args.cpu_seconds)
+        line["cpu_baseline"]["exchange_by_world"] = exchange_by_world(sizes, wl.get("cpu_worlds", (2, 4, 8)))
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()  # rank 0's CPU timings ran while the peers waited; close together
     if tr.device_status() != 0:
         raise SystemExit(f"device status {tr.device_status()} (timeout in a device wait)")
     xchg.close()
@@ -630,35 +784,65 @@ def pgx_arm(args):
 
 
 def trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world, steps=3):
-    """Per-layer exchange spans vs forward/backward on the device clock (CUDA events), in
-    the reference's timeline schema (timeline.py:34) and its overlap ratio (timeline.py:137)."""
+    """Per-layer exchange spans vs per-layer backward spans on the device clock (CUDA events),
+    in the reference's timeline schema (timeline.py:34) and its overlap ratio (timeline.py:137).
+    backward_layer(l) runs from the gradient w.r.t. the layer's output being ready (a tensor
+    hook on the module's output = the start of the layer's own backward kernels) to the layer's
+    parameter gradients being final (the exchange trigger, pipelined.py:91-95); send_trigger(l)
+    from that point to this rank's part of the layer exchange being done."""
     import torch
 
     from paper_1706_00095_b200.timeline import Recorder, compute_overlap, write_timeline_csv
 
     rec = Recorder(rank)
     bind.trace = []
-    marks = []
-    for _ in range(steps):
-        k = bind.k
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record()
-        xin = dev_x.to(torch.bfloat16, memory_format=torch.channels_last).sub_(128.0).mul_(1.0 / 64.0)
-        with torch.autocast("cuda", dtype=torch.bfloat16):
-            out = model(xin)
-        loss = model.loss(out, dev_y)
-        ev[1].record()
-        loss.backward()
-        ev[2].record()
-        bind.step_done()
-        marks.append((k, ev))
-    bind.drain()
-    torch.cuda.synchronize()
+    marks, starts, handles = [], [], []
+
+    def fwd_hook(l):
+        def hook(_m, _inp, out):
+            t = out[0] if isinstance(out, tuple) else out
+            if torch.is_tensor(t) and t.requires_grad:
+                k = bind.k
+
+                def on_grad(_g):
+                    ev = torch.cuda.Event(enable_timing=True)
+                    ev.record()
+                    starts.append((k, l, ev))
+                t.register_hook(on_grad)
+        return hook
+
+    for l, (mod, _) in enumerate(model.layers()):
+        handles.append(mod.register_forward_hook(fwd_hook(l)))
+    try:
+        for _ in range(steps):
+            k = bind.k
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record()
+            xin = dev_x.to(torch.bfloat16, memory_format=torch.channels_last).sub_(128.0).mul_(1.0 / 64.0)
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                out = model(xin)
+            loss = model.loss(out, dev_y)
+            ev[1].record()
+            loss.backward()
+            ev[2].record()
+            bind.step_done()
+            marks.append((k, ev))
+        bind.drain()
+        torch.cuda.synchronize()
+    finally:
+        for h in handles:
+            h.remove()
     t0 = marks[0][1][0]
     ns = lambda e: int(t0.elapsed_time(e) * 1e6)  # noqa: E731
+    ready = {(k, l): r0 for k, l, r0, _ in bind.trace}
     for k, ev in marks:
         rec.record("forward", k, -1, ns(ev[0]), ns(ev[1]))
-        rec.record("backward_layer", k, -1, ns(ev[1]), ns(ev[2]))
+    nlayer = 0
+    for k, l, ev in starts:
+        if (k, l) in ready:
+            a, b = ns(ev), ns(ready[(k, l)])
+            rec.record("backward_layer", k, l, min(a, b), b)
+            nlayer += 1
     tails = []
     for k, l, r0, e1 in bind.trace:
         rec.record("send_trigger", k, l, ns(r0), ns(e1))
@@ -670,8 +854,51 @@ def trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world, steps=3):
     if path:
         write_timeline_csv(rec.events, path.replace("{rank}", str(rank)))
     return {"overlap_ratio": compute_overlap(rec.events).overlap_ratio, "steps_traced": steps,
+            "backward_layer_spans": nlayer,
+            "definition": "comm time inside per-layer backward spans (layer output-grad ready -> param grads "
+                          "final) or forward, / comm time (timeline.py:137-175)",
             "exchange_tail_after_backward_ms": statistics.mean(tails), "schema": "timeline.py:34 CSV",
             "csv": path or None}
+
+
+def pipelined_vs_barrier(bind, step, dev_x, dev_y, world, steps=6):
+    """Wall time per eager step, pipelined (exchange launched from each layer's hook) vs the
+    phase-separated schedule (every exchange launched after the whole backward, the
+    reference's BarrierRank, barrier.py:24-141) with the same kernels: the reference's
+    `pipelined_over_barrier_wall` (harness.py:376-379)."""
+    import torch
+    import torch.distributed as dist
+
+    def run(deferred):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            if deferred:
+                bind.deferred = []
+            step(dev_x, dev_y)  # step() calls bind.step_done(); flush before it counts the step
+            if deferred:
+                bind.k -= 1
+                bind.flush()
+                bind.k += 1
+                bind.deferred = None
+        bind.drain()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    run(False)  # warm both schedules
+    run(True)
+    p_ms, b_ms = run(False), run(True)
+    return {"pipelined_ms_per_step": p_ms, "barrier_ms_per_step": b_ms, "pipelined_over_barrier_wall": p_ms / b_ms,
+            "barrier_schedule": "same kernels, every layer exchanged after the full backward (eager steps)"}
 
 
 def comparison_arm(args):
@@ -699,8 +926,8 @@ def comparison_arm(args):
     gb = B * world
     IMG = wl["image"]
     g = torch.Generator().manual_seed(42 + rank)
-    dev_x = torch.randint(0, 256, (B, 3, IMG, IMG), dtype=torch.uint8, generator=g).to(dev)
-    dev_y = torch.randint(0, 1000, (B,), dtype=torch.int64, generator=g).to(dev)
+    dev_x = torch.randint(0, 256, (B, wl.get("channels", 3), IMG, IMG), dtype=torch.uint8, generator=g).to(dev)
+    dev_y = torch.randint(0, wl.get("classes", 1000), (B,), dtype=torch.int64, generator=g).to(dev)
     params = [p for _, ps in model.layers() for p in ps]
     n = sum(p.numel() for p in params)
     if args.variant == "ddp":

@@ -64,14 +64,25 @@ def update_fast32(w, v, g, scale, lr, mu, wd):
 class ExchangeWorld:
     """fp32 buffers of `world` ranks for the CPU port of one pipelined iteration."""
 
-    def __init__(self, world: int, elems, seed: int = 42):
+    def __init__(self, world: int, elems, seed: int = 42, fast_fill: bool = False):
+        """fast_fill: numpy PCG64 draws instead of seeded_fill (timing runs at full model
+        sizes, where the arithmetic does not depend on the values and seeded_fill's
+        splitmix stream in numpy would take ~25 s for 8 AlexNet gradients)."""
         from . import pipesgd_oracle as O
 
         self.world, self.elems = world, [int(n) for n in elems]
         L = len(self.elems)
-        self.grad = [[O.seeded_fill(O.derived_seed(seed, r, l), n, 1e-3).astype(np.float32)
-                      for l, n in enumerate(self.elems)] for r in range(world)]
-        w0 = [O.seeded_fill(seed ^ l, n, 0.01).astype(np.float32) for l, n in enumerate(self.elems)]
+        if fast_fill:
+            rng = np.random.default_rng(seed)
+
+            def fill(_s, n, scale):
+                return (rng.standard_normal(n, dtype=np.float32) * np.float32(scale)).astype(np.float32)
+        else:
+            def fill(s, n, scale):
+                return O.seeded_fill(s, n, scale).astype(np.float32)
+        self.grad = [[fill(O.derived_seed(seed, r, l), n, 1e-3) for l, n in enumerate(self.elems)]
+                     for r in range(world)]
+        w0 = [fill(seed ^ l, n, 0.01) for l, n in enumerate(self.elems)]
         self.w = [[a.copy() for a in w0] for _ in range(world)]
         self.v = [np.zeros(n, np.float32) for n in self.elems]
         self.rx = [[np.zeros(n, np.float32) for n in self.elems] for _ in range(world)]

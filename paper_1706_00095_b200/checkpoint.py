@@ -85,8 +85,9 @@ def pack(layers, stream=None, out: torch.Tensor | None = None) -> tuple[torch.Te
     ptrs = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
     cnt = (C.c_uint64 * len(ts))(*counts)
     st = stream or torch.cuda.current_stream(dev)
-    _lib.call("pgx_ckpt_pack", ptrs, cnt, len(ts), ts[0].element_size(), C.c_void_p(img.data_ptr()),
-              words * 8, C.c_void_p(st.cuda_stream))
+    with torch.cuda.device(dev):  # the launch goes to the layers' device, whatever is current
+        _lib.call("pgx_ckpt_pack", ptrs, cnt, len(ts), ts[0].element_size(), C.c_void_p(img.data_ptr()),
+                  words * 8, C.c_void_p(st.cuda_stream))
     return img.view(torch.uint8), nbytes
 
 
@@ -187,8 +188,9 @@ def unpack_into(blob, layers, stream=None) -> None:
         img.copy_(host, non_blocking=True)
     ptrs = (C.c_void_p * len(layers))(*[t.data_ptr() for t in layers])
     cnt = (C.c_uint64 * len(layers))(*counts)
-    _lib.call("pgx_ckpt_unpack", C.c_void_p(img.data_ptr()), words * 8, cnt, len(layers),
-              layers[0].element_size(), ptrs, C.c_void_p(st.cuda_stream))
+    with torch.cuda.device(dev):
+        _lib.call("pgx_ckpt_unpack", C.c_void_p(img.data_ptr()), words * 8, cnt, len(layers),
+                  layers[0].element_size(), ptrs, C.c_void_p(st.cuda_stream))
     st.synchronize()  # the pinned staging buffer is released on return
 
 

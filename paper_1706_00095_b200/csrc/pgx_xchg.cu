@@ -489,23 +489,23 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
 // CTAs saturate NVLink (tools/probe_push.cu: 689 GB/s push from 16 CTAs), so the layer
 // leaves the other SMs to the backward kernels it overlaps with.
 constexpr int kBulkThreads = 256;
-constexpr int kBulkStage = 32768;  // bytes per ring slot
-constexpr int kBulkStages = 4;
-constexpr size_t kBulkSmem = (size_t)kBulkStages * kBulkStage + kBulkStages * sizeof(uint64_t);
+constexpr int kBulkStage = 32768;  // bytes per push ring slot
+constexpr int kBulkStages = 6;     // push ring: 192 KB, loads S-1 slots ahead
+constexpr int kBulkRing = kBulkStages * kBulkStage;
+constexpr int kOwnTile = 8192;     // bytes per owner input stream per tile
+constexpr int kOwnBars = 4;        // owner pipeline depth (max)
+constexpr size_t kBulkSmem = (size_t)kBulkRing + (kBulkStages + kOwnBars) * sizeof(uint64_t);
 constexpr int kBulkCtas = 24;      // default grid of a bulk layer
 
-__device__ __forceinline__ void tma_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
-__device__ __forceinline__ void tma_wait_read_all_but(int k) {
-  // k is a compile-time ring depth minus one at every call site
-  if (k >= 3)
-    asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
-  else if (k == 2)
-    asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
-  else if (k == 1)
-    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-  else
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+// Owner pipeline depth for N ranks: a stage holds N partial tiles + w + v; two output
+// tiles (all-gather sources) sit after the stages.
+__host__ __device__ constexpr int bulk_owner_stages(int N) {
+  return (kBulkRing - 2 * kOwnTile) / ((N + 2) * kOwnTile) < kOwnBars
+             ? (kBulkRing - 2 * kOwnTile) / ((N + 2) * kOwnTile)
+             : kOwnBars;
 }
+
+__device__ __forceinline__ void tma_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 
 struct BulkSeg {
   const uint8_t* src;
@@ -563,24 +563,45 @@ __device__ __forceinline__ void bulk_stream(const BulkSeg* segs, int nseg, uint8
   gload += n;
 }
 
+// The own gradient's part of [t0, t1) as one 16-byte-aligned source inside one piece, or null.
+template <class T>
+__device__ __forceinline__ const T* own_tile_src(const Pieces& P, uint64_t t0, uint64_t t1) {
+  uint64_t pb = 0;
+  for (int k = 0; k < P.n; ++k) {
+    const uint64_t pe = P.end[k];
+    if (t0 >= pb && t1 <= pe) {
+      const T* p = static_cast<const T*>(P.p[k]) + (t0 - pb);
+      return (reinterpret_cast<uintptr_t>(p) & 15) ? nullptr : p;
+    }
+    pb = pe;
+  }
+  return nullptr;
+}
+
 template <int N, class T>
 __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
   constexpr int W = VecT<T>::W;
   constexpr int S = kBulkStages;
-  constexpr uint64_t TE = kBulkStage / sizeof(T);  // elements per ring tile
+  constexpr int SO = bulk_owner_stages(N);
+  constexpr uint64_t TO = kOwnTile / sizeof(T);  // elements per owner tile
+  static_assert(SO >= 2, "owner pipeline needs two stages");
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
   extern __shared__ __align__(128) uint8_t ring[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + (size_t)S * kBulkStage);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kBulkRing);  // [S push][kOwnBars owner]
+  uint64_t* obars = bars + S;
+  T* outt = reinterpret_cast<T*>(ring + (size_t)SO * (N + 2) * kOwnTile);  // 2 output tiles
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
   if (threadIdx.x == 0) {
-    for (int k = 0; k < S; ++k) mbar_init(&bars[k], 1);
+    for (int k = 0; k < S + kOwnBars; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t gload = 0;  // thread 0's load counter (mbarrier phases)
+  uint32_t gload = 0, gown = 0;  // push / owner load counters (mbarrier phases; every thread tracks gown)
   const int me = a.rank;
+  const bool fast = sizeof(T) == 4 && a.mode == PGX_MODE_FAST32;
+  const bool upd = a.mode != PGX_MODE_SUM32;
   while (true) {
     const uint32_t it = claim(a.queue, &s_item) + a.item_begin;
     if (it >= a.item_end) break;
@@ -624,7 +645,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         st_release_sys(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
       }
     } else {
-      // ---- owner slab: fold N contributions in tree order, update, bulk all-gather
+      // ---- owner slab: TMA-fed fold of the N contributions in tree order, fused update,
+      // bulk all-gather.  Thread 0 keeps SO-1 tiles of every input stream in flight.
       const uint32_t c = it - a.push_items;
       const uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
       const uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
@@ -635,34 +657,106 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       }
       __syncthreads();
       cta_wait_flags(s_flags, N - 1, epoch, a.st);
-      const T* rxs = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
-      constexpr int U = (N <= 4 || sizeof(T) == 4) ? (N <= 4 ? 4 : 2) : 1;
-      uint32_t tile = 0;
-      for (uint64_t t0 = lo; t0 < hi; t0 += TE, ++tile) {
-        const uint64_t t1 = min(t0 + TE, hi);
-        T* stage = reinterpret_cast<T*>(ring + (size_t)(tile % S) * kBulkStage);
-        if (tile >= (uint32_t)S) {  // the slot's previous all-gather stores must have read it
-          if (threadIdx.x == 0) tma_wait_read_all_but(S - 1);
-          __syncthreads();
+      const T* rx0 = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl - (uint64_t)me * a.sl;
+      T* wme = static_cast<T*>(a.model[me]);
+      const uint32_t ntile = (uint32_t)((hi - lo + TO - 1) / TO);
+      auto stage = [&](uint32_t i) { return reinterpret_cast<T*>(ring + (size_t)((gown + i) % SO) * (N + 2) * kOwnTile); };
+      auto issue = [&](uint32_t i) {  // thread 0: every input stream of tile i
+        const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
+        const uint32_t body = (uint32_t)(((t1 - t0) * sizeof(T)) & ~uint64_t(15));
+        const T* og = own_tile_src<T>(a.g, t0, t1);
+        uint64_t* bar = &obars[(gown + i) % SO];
+        const uint32_t tx = body * ((N - 1) + (og ? 1 : 0) + (upd ? 1 : 0) + (fast ? 1 : 0));
+        mbar_expect_tx(bar, tx);
+        if (!body) return;
+        T* st = stage(i);
+        for (int s = 0; s < N; ++s) {
+          if (s == me) {
+            if (og) tma_load(st + s * TO, og, body, bar);
+          } else {
+            tma_load(st + s * TO, rx0 + (uint64_t)s * a.sl + t0, body, bar);
+          }
         }
+        if (upd) tma_load(st + N * TO, wme + t0, body, bar);
+        if (fast) tma_load(st + (N + 1) * TO, a.v + t0, body, bar);
+      };
+      if (threadIdx.x == 0)
+        for (uint32_t i = 0; i < min(ntile, (uint32_t)(SO - 1)); ++i) issue(i);
+      for (uint32_t i = 0; i < ntile; ++i) {
+        if (threadIdx.x == 0 && i + SO - 1 < ntile) issue(i + SO - 1);  // slot of tile i-1, consumed
+        const uint32_t g = gown + i;
+        mbar_wait(&obars[g % SO], (g / SO) & 1u);
+        const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
+        const uint64_t nfull = ((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W;  // vectors loaded by TMA
         const uint64_t nvec = (t1 - t0 + W - 1) / W;
-        for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
-          owner_vectors<N, T, U, false>(a, rxs + (t0 - lo), t0, t1, q0, nvec, stage);
-        __syncthreads();
-        if (N > 1 && threadIdx.x == 0) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
-          const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
-          if (body) {
-            for (int d = 1; d < N; ++d)
-              tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, stage, (uint32_t)body);
-            tma_commit();
+        const T* st = stage(i);
+        const bool og = own_tile_src<T>(a.g, t0, t1) != nullptr;
+        T* out = outt + (i & 1) * TO;
+        for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
+          const uint64_t e = t0 + q * W;
+          const int cnt = (int)min((uint64_t)W, t1 - e);
+          T vals[N][W], w[W];
+          float vv[W];
+          if (q < nfull) {
+#pragma unroll
+            for (int s = 0; s < N; ++s) {
+              if (s == me && !og)
+                grad_vec<T>(a.g, e, cnt, vals[s]);
+              else
+                memcpy(vals[s], st + s * TO + q * W, sizeof(vals[s]));
+            }
+            if (upd) memcpy(w, st + N * TO + q * W, sizeof(w));
+            if (fast) memcpy(vv, reinterpret_cast<const float*>(st + (N + 1) * TO) + q * W, sizeof(vv));
+          } else {  // ragged end of the layer (< 16 bytes): straight from global memory
+#pragma unroll
+            for (int s = 0; s < N; ++s) {
+              if (s == me)
+                grad_vec<T>(a.g, e, cnt, vals[s]);
+              else
+                ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt, vals[s]);
+            }
+            if (upd) ld_vec<T>(wme + e, cnt, w);
+            if (fast) ld_vec<float>(a.v + e, cnt, vv);
           }
-          for (int d = 1; d < N; ++d) {  // ragged end of the layer (< 16 bytes)
-            uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
-            for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(stage)[b];
+          if (!upd) {
+#pragma unroll
+            for (int k = 0; k < W; ++k) w[k] = T(0);
+          }
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            T col[N];
+#pragma unroll
+            for (int s = 0; s < N; ++s) col[s] = vals[s][k];
+            T gsum;
+            if constexpr (sizeof(T) == 8)
+              gsum = tree_sum<N>(col, AddF64{});
+            else
+              gsum = tree_sum<N>(col, AddF32{});
+            w[k] = apply_update<T>(w[k], gsum, vv[k], a);
+          }
+          st_vec<T>(wme + e, cnt, w);
+          if (fast) st_vec<float>(a.v + e, cnt, vv);
+          st_vec<T>(out + q * W, cnt, w);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (N > 1) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+            const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
+            if (body) {
+              for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, out, (uint32_t)body);
+              tma_commit();
+            }
+            for (int d = 1; d < N; ++d) {  // ragged end of the layer (< 16 bytes)
+              uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
+              for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(out)[b];
+            }
+            tma_wait_read_1();  // tile i-1's all-gather has read the other output tile
           }
         }
+        __syncthreads();  // output tile (i+1)&1 and stage slot i%SO are free again
       }
+      gown += ntile;
       if (N > 1 && threadIdx.x == 0) {
         tma_wait_all();
         asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -352,6 +352,7 @@ class ModuleBinding:
         self._tstream = None
         self.trace = None                # list -> record (iteration, layer, ready_event, done_event)
         self.events: dict = {}
+        self.deferred = None             # list -> phase-separated schedule: hooks queue, flush() launches
 
     def _make_hook(self, l):
         def hook(_p):
@@ -360,6 +361,12 @@ class ModuleBinding:
             if self._pending[l] < len(params):
                 return
             self._pending[l] = 0
+            if self.deferred is not None:  # barrier schedule (barrier.py:24-141): exchange after backward
+                self.deferred.append((l, [p.grad if p.grad.is_contiguous() else p.grad.contiguous()
+                                          for p in params]))
+                for p in params:
+                    p.grad = None
+                return
             compute = torch.cuda.current_stream(self.x.tr.device)
             xs = self.x.stream_for(l)
             xs.wait_stream(compute)
@@ -414,6 +421,20 @@ class ModuleBinding:
                 self.x.gate(l, self.k - 1)
                 self.gpu_launches += 1
         return pre_hook
+
+    def flush(self) -> None:
+        """Phase-separated schedule (the reference's BarrierRank, barrier.py:24-141, as the
+        comparison row): launch every queued layer exchange now that backward has finished,
+        in emission order, each behind the whole backward."""
+        if not self.deferred:
+            return
+        compute = torch.cuda.current_stream(self.x.tr.device)
+        for l, pieces in self.deferred:
+            xs = self.x.stream_for(l)
+            xs.wait_stream(compute)
+            self.x.launch(l, self.k, pieces, stream=xs)
+            self.gpu_launches += 1
+        self.deferred.clear()
 
     def step_done(self) -> None:
         """Call once per iteration after backward(); raises if a device wait expired."""

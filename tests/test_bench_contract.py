@@ -39,3 +39,19 @@ def test_gpu_arm_refuses_without_a_gpu():
     assert not any(ln.startswith("{") and '"value"' in ln for ln in r.stdout.splitlines()), \
         "the GPU arm must not print a number without a GPU"
     assert r.returncode != 0
+
+
+def test_reference_arm_times_the_reference_engine_for_configs0():
+    """configs[0] (LeNet, 2 ranks): the reference arm measures full steps and the reference's
+    own PipelinedRank exchange (baseline/_ref) beside the C port — no extrapolated samples."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "pipesgd")):
+        pytest.skip("reference not installed in baseline/_ref")
+    r = _run("--impl", "reference", "--workload", "lenet", "--gpus", "2", "--steps", "2", "--warmup", "1")
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    cb = d["cpu_baseline"]
+    assert d["n_gpus"] == 2 and cb["steps_measured"] == 2
+    assert d["config"]["workload"] == "lenet5_b64_synthetic_28" and d["config"]["global_batch"] == 64
+    ref = cb["reference_engine_exchange"]
+    assert ref["ms"] > 0 and ref["iterations"] == 2
+    assert abs(d["ms_per_step"] - (1e3 * 64 / d["value"])) < 1e-6 * d["ms_per_step"]

@@ -110,3 +110,17 @@ def test_exchange_checkpoint_roundtrip(tmp_path):
     assert O.ckpt_load(open(path, "rb").read())[2].tobytes() == saved[2].cpu().double().numpy().tobytes()
     x.close()
     tr.close()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_pack_unpack_on_a_non_current_device():
+    """Layers on cuda:1 while cuda:0 is current: the kernels must launch on the layers' device."""
+    from paper_1706_00095_b200.checkpoint import load_model_bytes, serialize_model
+
+    torch.cuda.set_device(0)
+    dev = [torch.from_numpy(a.copy()).to("cuda:1") for a in small_layers()]
+    blob = serialize_model(dev)
+    assert blob == G["ckpt_small_blob"].tobytes()
+    back = load_model_bytes(blob, device="cuda:1")
+    for a, t in zip(small_layers(), back.layers):
+        assert t.device.index == 1 and t.cpu().numpy().tobytes() == a.astype(np.float64).tobytes()

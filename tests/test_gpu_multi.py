@@ -159,49 +159,15 @@ def test_host_engine_over_ipc_matches_sequential(pattern):
 
 
 def _lenet():
-    import torch.nn as nn
-
-    class LeNet(nn.Module):  # Caffe lenet_train_test.prototxt: 520 / 25,050 / 400,500 / 5,010 params
-        def __init__(self):
-            super().__init__()
-            self.conv1 = nn.Conv2d(1, 20, 5)
-            self.conv2 = nn.Conv2d(20, 50, 5)
-            self.ip1 = nn.Linear(800, 500)
-            self.ip2 = nn.Linear(500, 10)
-
-        def forward(self, x):
-            x = torch.max_pool2d(self.conv1(x), 2, 2)
-            x = torch.max_pool2d(self.conv2(x), 2, 2)
-            return self.ip2(torch.relu(self.ip1(x.flatten(1))))
-
-        def layers(self):
-            return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.ip1, self.ip2)]
+    from workloads import LeNet
 
     return LeNet()
 
 
 def _cifar10_quick():
-    import torch.nn as nn
+    from workloads import Cifar10Quick
 
-    class Quick(nn.Module):  # Caffe cifar10_quick: 2,432 / 25,632 / 51,264 / 65,600 / 650 params
-        def __init__(self):
-            super().__init__()
-            self.conv1 = nn.Conv2d(3, 32, 5, padding=2)
-            self.conv2 = nn.Conv2d(32, 32, 5, padding=2)
-            self.conv3 = nn.Conv2d(32, 64, 5, padding=2)
-            self.ip1 = nn.Linear(1024, 64)
-            self.ip2 = nn.Linear(64, 10)
-
-        def forward(self, x):
-            x = torch.relu(torch.max_pool2d(self.conv1(x), 3, 2, ceil_mode=True))
-            x = torch.nn.functional.avg_pool2d(torch.relu(self.conv2(x)), 3, 2, ceil_mode=True)
-            x = torch.nn.functional.avg_pool2d(torch.relu(self.conv3(x)), 3, 2, ceil_mode=True)
-            return self.ip2(self.ip1(x.flatten(1)))
-
-        def layers(self):
-            return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.conv3, self.ip1, self.ip2)]
-
-    return Quick()
+    return Cifar10Quick()
 
 
 def _model_worker(rank, world, port, which, variant, gate, q):

@@ -157,6 +157,53 @@ class GoogLeNet(nn.Module):
         return [(m, [m.weight, m.bias]) for m in mods]
 
 
+class LeNet(nn.Module):
+    """Caffe lenet_train_test.prototxt (configs[0], the CPU reference's own workload shape):
+    520 / 25,050 / 400,500 / 5,010 params."""
+
+    def __init__(self):
+        super().__init__()
+        self.conv1 = nn.Conv2d(1, 20, 5)
+        self.conv2 = nn.Conv2d(20, 50, 5)
+        self.ip1 = nn.Linear(800, 500)
+        self.ip2 = nn.Linear(500, 10)
+
+    def forward(self, x):
+        x = F.max_pool2d(self.conv1(x), 2, 2)
+        x = F.max_pool2d(self.conv2(x), 2, 2)
+        return self.ip2(torch.relu(self.ip1(x.flatten(1))))
+
+    def loss(self, out, y):
+        return F.cross_entropy(out.float(), y)
+
+    def layers(self):
+        return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.ip1, self.ip2)]
+
+
+class Cifar10Quick(nn.Module):
+    """Caffe cifar10_quick (configs[1]): 2,432 / 25,632 / 51,264 / 65,600 / 650 params."""
+
+    def __init__(self):
+        super().__init__()
+        self.conv1 = nn.Conv2d(3, 32, 5, padding=2)
+        self.conv2 = nn.Conv2d(32, 32, 5, padding=2)
+        self.conv3 = nn.Conv2d(32, 64, 5, padding=2)
+        self.ip1 = nn.Linear(1024, 64)
+        self.ip2 = nn.Linear(64, 10)
+
+    def forward(self, x):
+        x = torch.relu(F.max_pool2d(self.conv1(x), 3, 2, ceil_mode=True))
+        x = F.avg_pool2d(torch.relu(self.conv2(x)), 3, 2, ceil_mode=True)
+        x = F.avg_pool2d(torch.relu(self.conv3(x)), 3, 2, ceil_mode=True)
+        return self.ip2(self.ip1(x.flatten(1)))
+
+    def loss(self, out, y):
+        return F.cross_entropy(out.float(), y)
+
+    def layers(self):
+        return [(m, [m.weight, m.bias]) for m in (self.conv1, self.conv2, self.conv3, self.ip1, self.ip2)]
+
+
 WORKLOADS = {
     "alexnet": dict(cls=AlexNet, image=227, global_batch=256, scaling="strong",
                     hyper=dict(lr=0.01, momentum=0.9, weight_decay=5e-4),
@@ -164,4 +211,11 @@ WORKLOADS = {
     "googlenet": dict(cls=GoogLeNet, image=224, per_gpu_batch=32, scaling="weak",
                       hyper=dict(lr=0.01, momentum=0.9, weight_decay=2e-4),
                       metric="GoogLeNet images/sec (B=32 per GPU, synthetic 224x224), per-layer gradient exchange"),
+    "lenet": dict(cls=LeNet, image=28, channels=1, classes=10, global_batch=64, scaling="strong",
+                  hyper=dict(lr=0.01, momentum=0.0, weight_decay=0.0), reference_world=2,
+                  metric="LeNet-5 images/sec (B=64 global, synthetic 28x28), per-layer gradient exchange"),
+    "cifar10_quick": dict(cls=Cifar10Quick, image=32, classes=10, per_gpu_batch=100, scaling="weak",
+                          hyper=dict(lr=0.001, momentum=0.9, weight_decay=0.004), reference_world=4,
+                          metric="cifar10_quick images/sec (B=100 per GPU, synthetic 32x32), per-layer gradient "
+                                 "exchange"),
 }
