@@ -476,6 +476,16 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
   retire(a.queue);
 }
 
+// Debug timeline (pgx_xchg_set_trace): item `it` -> [claim, mid, end, smid], thread 0 only.
+__device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slot) {
+  if (a.trace && threadIdx.x == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    a.trace[(uint64_t)it * 4 + slot] = globaltimer_ns();
+    a.trace[(uint64_t)it * 4 + 3] = sm;
+  }
+}
+
 // ============================================================== TWOSHOT_BULK
 // The two-shot schedule with every NVLink byte moved by the Tensor Memory Accelerator on
 // a capped grid (the large-layer variant): per CTA one thread streams a slab through a
@@ -606,6 +616,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
     const uint32_t it = claim(a.queue, &s_item) + a.item_begin;
     if (it >= a.item_end) break;
     if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // ring: generic <-> async
+    trace_stamp(a, it, 0);
     if (N > 1 && it < a.push_items) {
       // ---- reduce-scatter: slab c of owner j's shard -> j's rx[parity][me]
       constexpr int NP = N > 1 ? N - 1 : 1;
@@ -637,6 +648,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         pb = pe;
       }
       if (threadIdx.x == 0 && nseg) bulk_stream(segs, nseg, ring, bars, gload);
+      trace_stamp(a, it, 1);
       __syncthreads();
       if (threadIdx.x == 0) {
         tma_wait_all();                                      // the slab's bulk writes are done
@@ -644,6 +656,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         fence_acq_rel_sys();
         st_release_sys(a.rxflags[j] + (uint64_t)me * a.C + c, epoch);
       }
+      trace_stamp(a, it, 2);
     } else {
       // ---- owner slab: TMA-fed fold of the N contributions in tree order, fused update,
       // bulk all-gather.  Thread 0 keeps SO-1 tiles of every input stream in flight.
@@ -657,6 +670,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       }
       __syncthreads();
       cta_wait_flags(s_flags, N - 1, epoch, a.st);
+      trace_stamp(a, it, 1);
       const T* rx0 = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl - (uint64_t)me * a.sl;
       T* wme = static_cast<T*>(a.model[me]);
       const uint32_t ntile = (uint32_t)((hi - lo + TO - 1) / TO);
@@ -763,20 +777,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         fence_acq_rel_sys();
         for (int d = 1; d < N; ++d) red_release_sys_add(a.mflags[(me + d) % N] + a.layer, 1u);
       }
+      trace_stamp(a, it, 2);
     }
   }
   if (threadIdx.x == 0) tma_wait_all();
   retire(a.queue);
-}
-
-// Debug timeline (pgx_xchg_set_trace): item `it` -> [claim, mid, end, smid], thread 0 only.
-__device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slot) {
-  if (a.trace && threadIdx.x == 0) {
-    uint32_t sm;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    a.trace[(uint64_t)it * 4 + slot] = globaltimer_ns();
-    a.trace[(uint64_t)it * 4 + 3] = sm;
-  }
 }
 
 // ============================================================== ONESHOT

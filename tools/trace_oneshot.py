@@ -1,7 +1,9 @@
-"""Per-work-item device timeline of one ONESHOT exchange (pgx_xchg_set_trace): where the
-latency of a 1 MB layer goes (push / fence+flag / wait / fold), every rank.
+"""Per-work-item device timeline of one exchange (pgx_xchg_set_trace; ONESHOT and
+TWOSHOT_BULK are instrumented): where the time of a layer goes (push / fence+flag / wait /
+fold), every rank.
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/trace_oneshot.py [--kb 1024]
+        [--variant oneshot|twoshot_bulk] [--ctas 0]
 """
 
 from __future__ import annotations
@@ -26,6 +28,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kb", type=int, default=1024)
     ap.add_argument("--chunk", type=int, default=16384)
+    ap.add_argument("--variant", default="oneshot")
+    ap.add_argument("--ctas", type=int, default=0)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -33,11 +37,14 @@ def main():
     dist.init_process_group("gloo", rank=rank, world_size=world)
     n = args.kb * 256
     tr = DistTransport(rank, world, local, timeout_s=20.0)
-    x = DeviceExchange(tr, [n], mode="fast32", variant="oneshot", chunk_elems=args.chunk, lr=0.01, momentum=0.9)
+    x = DeviceExchange(tr, [n], mode="fast32", variant=args.variant, chunk_elems=args.chunk, lr=0.01, momentum=0.9,
+                       max_ctas=args.ctas)
     tr.barrier()
     x.connect()
     g = torch.randn(n, device="cuda") * 1e-3
-    C_ = -(-n // x.layer_plan(0)[0])
+    ch = x.layer_plan(0)[0]
+    sl = ((n + world - 1) // world + 3) // 4 * 4  # two-shot shard (pgx_xchg_create)
+    C_ = -(-n // ch) if args.variant == "oneshot" else -(-sl // ch)
     items = (world - 1) * C_ + C_
     buf = torch.zeros(items * 4, dtype=torch.int64, device="cuda")
     out = []
@@ -71,7 +78,10 @@ def main():
                                                        max(o[1] for o in own) / 1e3],
                         "owner_end_us_med_max": [statistics.median(o[2] for o in own) / 1e3,
                                                  max(o[2] for o in own) / 1e3],
-                        "items": items, "chunk": x.layer_plan(0)[0], "ctas": x.layer_plan(0)[1]})
+                        "items": items, "chunk": x.layer_plan(0)[0], "ctas": x.layer_plan(0)[1],
+                        "variant": args.variant, "kb": args.kb,
+                        "push_item_us_med": statistics.median(p[2] - p[0] for p in push) / 1e3,
+                        "owner_fold_us_med": statistics.median(o[2] - o[1] for o in own) / 1e3})
     allr = [None] * world
     dist.all_gather_object(allr, out)
     if rank == 0:
