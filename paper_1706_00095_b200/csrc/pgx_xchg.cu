@@ -500,22 +500,29 @@ __device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slo
 // leaves the other SMs to the backward kernels it overlaps with.
 constexpr int kBulkThreads = 256;
 constexpr int kBulkStage = 32768;  // bytes per push ring slot
-constexpr int kBulkStages = 6;     // push ring: 192 KB, loads S-1 slots ahead
+constexpr int kBulkStages = 7;     // push ring: 224 KB
+constexpr int kBulkAhead = 3;      // push loads in flight; the other slots hold stores in flight
 constexpr int kBulkRing = kBulkStages * kBulkStage;
-constexpr int kOwnTile = 8192;     // bytes per owner input stream per tile
-constexpr int kOwnBars = 4;        // owner pipeline depth (max)
+constexpr int kOwnOut = 8;         // owner output ring (all-gather sources): stores in flight
+constexpr int kOwnBars = 4;        // owner input pipeline depth (max)
 constexpr size_t kBulkSmem = (size_t)kBulkRing + (kBulkStages + kOwnBars) * sizeof(uint64_t);
 constexpr int kBulkCtas = 24;      // default grid of a bulk layer
 
-// Owner pipeline depth for N ranks: a stage holds N partial tiles + w + v; two output
-// tiles (all-gather sources) sit after the stages.
+// Owner tiles: bytes per input stream per tile, and the input pipeline depth for N ranks
+// (a stage holds N partial tiles + w + v; the output ring sits after the stages).  A remote
+// bulk store releases its shared-memory source only about one NVLink round trip after it
+// was issued (measured, r5d: one store in flight per CTA = 5 GB/s), so both rings keep
+// several stores in flight.
+__host__ __device__ constexpr int bulk_owner_tile(int N) { return N <= 4 ? 8192 : 4096; }
 __host__ __device__ constexpr int bulk_owner_stages(int N) {
-  return (kBulkRing - 2 * kOwnTile) / ((N + 2) * kOwnTile) < kOwnBars
-             ? (kBulkRing - 2 * kOwnTile) / ((N + 2) * kOwnTile)
+  return (kBulkRing - kOwnOut * bulk_owner_tile(N)) / ((N + 2) * bulk_owner_tile(N)) < kOwnBars
+             ? (kBulkRing - kOwnOut * bulk_owner_tile(N)) / ((N + 2) * bulk_owner_tile(N))
              : kOwnBars;
 }
 
 __device__ __forceinline__ void tma_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(K) : "memory"); }
 
 struct BulkSeg {
   const uint8_t* src;
@@ -538,12 +545,13 @@ __device__ __forceinline__ uint32_t bulk_tile(const BulkSeg* s, int n, uint32_t 
   return 0;
 }
 
-// One thread: copy the segments through the ring (loads S-1 tiles ahead).  `gload`
-// counts every load this CTA ever issued: load g uses slot g % S at mbarrier phase
-// (g / S) & 1.  Returns with stores possibly in flight (caller: wait_group 0).
+// One thread: copy the segments through the ring, kBulkAhead loads and up to
+// S - kBulkAhead stores in flight.  `gload` counts every load this CTA ever issued: load g
+// uses slot g % S at mbarrier phase (g / S) & 1.  Returns with stores possibly in flight
+// (caller: wait_group 0).
 __device__ __forceinline__ void bulk_stream(const BulkSeg* segs, int nseg, uint8_t* ring, uint64_t* bars,
                                             uint32_t& gload) {
-  constexpr int S = kBulkStages;
+  constexpr int S = kBulkStages, L = kBulkAhead;
   uint32_t n = 0;
   for (int k = 0; k < nseg; ++k) n += (uint32_t)((segs[k].bytes + kBulkStage - 1) / kBulkStage);
   auto load = [&](uint32_t j) {
@@ -554,7 +562,7 @@ __device__ __forceinline__ void bulk_stream(const BulkSeg* segs, int nseg, uint8
     mbar_expect_tx(&bars[s], b);
     tma_load(ring + (size_t)s * kBulkStage, src, b, &bars[s]);
   };
-  const uint32_t pre = min(n, (uint32_t)(S - 1));
+  const uint32_t pre = min(n, (uint32_t)L);
   for (uint32_t j = 0; j < pre; ++j) load(j);
   for (uint32_t j = 0; j < n; ++j) {
     const uint32_t g = gload + j;
@@ -565,9 +573,9 @@ __device__ __forceinline__ void bulk_stream(const BulkSeg* segs, int nseg, uint8
     const uint32_t b = bulk_tile(segs, nseg, j, &src, &dst);
     tma_store(dst, ring + (size_t)s * kBulkStage, b);
     tma_commit();
-    if (j + S - 1 < n) {
-      tma_wait_read_1();  // slot (j+S-1)%S was read by the store of tile j-1
-      load(j + S - 1);
+    if (j + L < n) {
+      tma_wait_read<S - L>();  // slot (j+L)%S was read by the store of tile j+L-S
+      load(j + L);
     }
   }
   gload += n;
@@ -593,14 +601,15 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
   constexpr int W = VecT<T>::W;
   constexpr int S = kBulkStages;
   constexpr int SO = bulk_owner_stages(N);
-  constexpr uint64_t TO = kOwnTile / sizeof(T);  // elements per owner tile
+  constexpr int TB = bulk_owner_tile(N);          // bytes per owner input stream per tile
+  constexpr uint64_t TO = TB / sizeof(T);         // elements per owner tile
   static_assert(SO >= 2, "owner pipeline needs two stages");
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
   extern __shared__ __align__(128) uint8_t ring[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kBulkRing);  // [S push][kOwnBars owner]
   uint64_t* obars = bars + S;
-  T* outt = reinterpret_cast<T*>(ring + (size_t)SO * (N + 2) * kOwnTile);  // 2 output tiles
+  T* outt = reinterpret_cast<T*>(ring + (size_t)SO * (N + 2) * TB);  // kOwnOut output tiles
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
   if (threadIdx.x == 0) {
@@ -674,7 +683,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       const T* rx0 = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl - (uint64_t)me * a.sl;
       T* wme = static_cast<T*>(a.model[me]);
       const uint32_t ntile = (uint32_t)((hi - lo + TO - 1) / TO);
-      auto stage = [&](uint32_t i) { return reinterpret_cast<T*>(ring + (size_t)((gown + i) % SO) * (N + 2) * kOwnTile); };
+      auto stage = [&](uint32_t i) { return reinterpret_cast<T*>(ring + (size_t)((gown + i) % SO) * (N + 2) * TB); };
       auto issue = [&](uint32_t i) {  // thread 0: every input stream of tile i
         const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
         const uint32_t body = (uint32_t)(((t1 - t0) * sizeof(T)) & ~uint64_t(15));
@@ -697,15 +706,19 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       if (threadIdx.x == 0)
         for (uint32_t i = 0; i < min(ntile, (uint32_t)(SO - 1)); ++i) issue(i);
       for (uint32_t i = 0; i < ntile; ++i) {
-        if (threadIdx.x == 0 && i + SO - 1 < ntile) issue(i + SO - 1);  // slot of tile i-1, consumed
+        if (threadIdx.x == 0) {
+          if (i + SO - 1 < ntile) issue(i + SO - 1);  // slot of tile i-1, consumed
+          if (N > 1 && i >= (uint32_t)kOwnOut) tma_wait_read<kOwnOut - 1>();  // tile i-kOwnOut's sources read
+        }
         const uint32_t g = gown + i;
         mbar_wait(&obars[g % SO], (g / SO) & 1u);
+        __syncthreads();  // output slot i % kOwnOut is free
         const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
         const uint64_t nfull = ((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W;  // vectors loaded by TMA
         const uint64_t nvec = (t1 - t0 + W - 1) / W;
         const T* st = stage(i);
         const bool og = own_tile_src<T>(a.g, t0, t1) != nullptr;
-        T* out = outt + (i & 1) * TO;
+        T* out = outt + (i % kOwnOut) * TO;
         for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
           const uint64_t e = t0 + q * W;
           const int cnt = (int)min((uint64_t)W, t1 - e);
@@ -765,10 +778,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
               uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
               for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(out)[b];
             }
-            tma_wait_read_1();  // tile i-1's all-gather has read the other output tile
           }
         }
-        __syncthreads();  // output tile (i+1)&1 and stage slot i%SO are free again
       }
       gown += ntile;
       if (N > 1 && threadIdx.x == 0) {
