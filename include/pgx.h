@@ -309,7 +309,7 @@ int pgx_xchg_layer_plan(pgx_xchg* x, int layer, uint64_t* chunk_elems_out, int* 
 /* TWOSHOT_CE: how many pipelined parts this rank's owner shard of `layer` is split into
  * (1 for every other variant). */
 int pgx_xchg_layer_parts(pgx_xchg* x, int layer, int* parts_out);
-/* Debug timeline: when `device_buffer` (u64 [items][4]) is non-NULL, instrumented kernels
+/* Debug timeline: when `device_buffer` (u64 [items][8]) is non-NULL, instrumented kernels
  * (ONESHOT) stamp each work item's claim / mid / end globaltimer ns and SM id into it.
  * NULL turns it off (the default: one predicated-off branch per item). */
 int pgx_xchg_set_trace(pgx_xchg* x, void* device_buffer);

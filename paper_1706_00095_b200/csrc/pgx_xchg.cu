@@ -476,13 +476,14 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
   retire(a.queue);
 }
 
-// Debug timeline (pgx_xchg_set_trace): item `it` -> [claim, mid, end, smid], thread 0 only.
+// Debug timeline (pgx_xchg_set_trace): item `it` -> [claim, mid, end, smid, 4 kernel-specific
+// accumulators], thread 0 only.
 __device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slot) {
   if (a.trace && threadIdx.x == 0) {
     uint32_t sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    a.trace[(uint64_t)it * 4 + slot] = globaltimer_ns();
-    a.trace[(uint64_t)it * 4 + 3] = sm;
+    a.trace[(uint64_t)it * 8 + slot] = globaltimer_ns();
+    a.trace[(uint64_t)it * 8 + 3] = sm;
   }
 }
 
@@ -705,14 +706,21 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       };
       if (threadIdx.x == 0)
         for (uint32_t i = 0; i < min(ntile, (uint32_t)(SO - 1)); ++i) issue(i);
+      unsigned long long t_in = 0, t_out = 0, t_bar = 0, t_x;
+      const bool tr = a.trace && threadIdx.x == 0;
       for (uint32_t i = 0; i < ntile; ++i) {
         if (threadIdx.x == 0) {
           if (i + SO - 1 < ntile) issue(i + SO - 1);  // slot of tile i-1, consumed
+          if (tr) t_x = globaltimer_ns();
           if (N > 1 && i >= (uint32_t)kOwnOut) tma_wait_read<kOwnOut - 1>();  // tile i-kOwnOut's sources read
+          if (tr) t_out += globaltimer_ns() - t_x;
         }
         const uint32_t g = gown + i;
+        if (tr) t_x = globaltimer_ns();
         mbar_wait(&obars[g % SO], (g / SO) & 1u);
+        if (tr) t_in += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         __syncthreads();  // output slot i % kOwnOut is free
+        if (tr) t_bar += globaltimer_ns() - t_x;
         const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
         const uint64_t nfull = ((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W;  // vectors loaded by TMA
         const uint64_t nvec = (t1 - t0 + W - 1) / W;
@@ -765,10 +773,13 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
           if (fast) st_vec<float>(a.v + e, cnt, vv);
           st_vec<T>(out + q * W, cnt, w);
         }
+        // every writer orders its generic smem writes before the async proxy's reads
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (tr) t_x = globaltimer_ns();
         __syncthreads();
+        if (tr) t_bar += globaltimer_ns() - t_x;
         if (threadIdx.x == 0) {
           if (N > 1) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
             const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
             if (body) {
               for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, out, (uint32_t)body);
@@ -782,6 +793,12 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         }
       }
       gown += ntile;
+      if (tr) {
+        a.trace[(uint64_t)it * 8 + 4] = t_in;
+        a.trace[(uint64_t)it * 8 + 5] = t_out;
+        a.trace[(uint64_t)it * 8 + 6] = t_bar;
+        a.trace[(uint64_t)it * 8 + 7] = ntile;
+      }
       if (N > 1 && threadIdx.x == 0) {
         tma_wait_all();
         asm volatile("fence.proxy.async.global;" ::: "memory");

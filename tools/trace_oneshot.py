@@ -46,7 +46,7 @@ def main():
     sl = ((n + world - 1) // world + 3) // 4 * 4  # two-shot shard (pgx_xchg_create)
     C_ = -(-n // ch) if args.variant == "oneshot" else -(-sl // ch)
     items = (world - 1) * C_ + C_
-    buf = torch.zeros(items * 4, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(items * 8, dtype=torch.int64, device="cuda")
     out = []
     for it in range(8):
         traced = it >= 5
@@ -64,7 +64,7 @@ def main():
         e1.record(x.stream)
         torch.cuda.synchronize()
         if traced:
-            t = buf.view(items, 4).cpu().tolist()
+            t = buf.view(items, 8).cpu().tolist()
             t0 = min(r[0] for r in t if r[0])
             push = [(r[0] - t0, r[1] - t0, r[2] - t0) for r in t[: (world - 1) * C_]]
             own = [(r[0] - t0, r[1] - t0, r[2] - t0) for r in t[(world - 1) * C_:]]
@@ -81,7 +81,10 @@ def main():
                         "items": items, "chunk": x.layer_plan(0)[0], "ctas": x.layer_plan(0)[1],
                         "variant": args.variant, "kb": args.kb,
                         "push_item_us_med": statistics.median(p[2] - p[0] for p in push) / 1e3,
-                        "owner_fold_us_med": statistics.median(o[2] - o[1] for o in own) / 1e3})
+                        "owner_fold_us_med": statistics.median(o[2] - o[1] for o in own) / 1e3,
+                        "owner_acc_us_med": [statistics.median(r[k] for r in t[(world - 1) * C_:]) / 1e3
+                                             for k in (4, 5, 6)],
+                        "owner_tiles": statistics.median(r[7] for r in t[(world - 1) * C_:])})
     allr = [None] * world
     dist.all_gather_object(allr, out)
     if rank == 0:
