@@ -706,21 +706,20 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       };
       if (threadIdx.x == 0)
         for (uint32_t i = 0; i < min(ntile, (uint32_t)(SO - 1)); ++i) issue(i);
-      unsigned long long t_in = 0, t_out = 0, t_bar = 0, t_x;
+      unsigned long long t_in = 0, t_iss = 0, t_comp = 0, t_st = 0, t_x = 0;
       const bool tr = a.trace && threadIdx.x == 0;
       for (uint32_t i = 0; i < ntile; ++i) {
         if (threadIdx.x == 0) {
-          if (i + SO - 1 < ntile) issue(i + SO - 1);  // slot of tile i-1, consumed
           if (tr) t_x = globaltimer_ns();
+          if (i + SO - 1 < ntile) issue(i + SO - 1);  // slot of tile i-1, consumed
           if (N > 1 && i >= (uint32_t)kOwnOut) tma_wait_read<kOwnOut - 1>();  // tile i-kOwnOut's sources read
-          if (tr) t_out += globaltimer_ns() - t_x;
+          if (tr) t_iss += globaltimer_ns() - t_x;
         }
         const uint32_t g = gown + i;
         if (tr) t_x = globaltimer_ns();
         mbar_wait(&obars[g % SO], (g / SO) & 1u);
-        if (tr) t_in += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         __syncthreads();  // output slot i % kOwnOut is free
-        if (tr) t_bar += globaltimer_ns() - t_x;
+        if (tr) t_in += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
         const uint64_t nfull = ((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W;  // vectors loaded by TMA
         const uint64_t nvec = (t1 - t0 + W - 1) / W;
@@ -775,9 +774,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         }
         // every writer orders its generic smem writes before the async proxy's reads
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (tr) t_x = globaltimer_ns();
         __syncthreads();
-        if (tr) t_bar += globaltimer_ns() - t_x;
+        if (tr) t_comp += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         if (threadIdx.x == 0) {
           if (N > 1) {
             const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
@@ -790,14 +788,15 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
               for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(out)[b];
             }
           }
+          if (tr) t_st += globaltimer_ns() - t_x;
         }
       }
       gown += ntile;
       if (tr) {
-        a.trace[(uint64_t)it * 8 + 4] = t_in;
-        a.trace[(uint64_t)it * 8 + 5] = t_out;
-        a.trace[(uint64_t)it * 8 + 6] = t_bar;
-        a.trace[(uint64_t)it * 8 + 7] = ntile;
+        a.trace[(uint64_t)it * 8 + 4] = t_in;    // input tiles + barrier
+        a.trace[(uint64_t)it * 8 + 5] = t_iss;   // issuing the loads (+ output-ring wait)
+        a.trace[(uint64_t)it * 8 + 6] = t_comp;  // fold + update + barrier
+        a.trace[(uint64_t)it * 8 + 7] = t_st;    // issuing the all-gather stores
       }
       if (N > 1 && threadIdx.x == 0) {
         tma_wait_all();
