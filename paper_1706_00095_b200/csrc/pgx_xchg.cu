@@ -504,21 +504,21 @@ constexpr int kBulkStage = 32768;  // bytes per push ring slot
 constexpr int kBulkStages = 7;     // push ring: 224 KB
 constexpr int kBulkAhead = 3;      // push loads in flight; the other slots hold stores in flight
 constexpr int kBulkRing = kBulkStages * kBulkStage;
-constexpr int kOwnOut = 8;         // owner output ring (all-gather sources): stores in flight
-constexpr int kOwnBars = 4;        // owner input pipeline depth (max)
+constexpr int kOwnBars = 8;        // owner pipeline depth (max)
 constexpr size_t kBulkSmem = (size_t)kBulkRing + (kBulkStages + kOwnBars) * sizeof(uint64_t);
 constexpr int kBulkCtas = 24;      // default grid of a bulk layer
 
-// Owner tiles: bytes per input stream per tile, and the input pipeline depth for N ranks
-// (a stage holds N partial tiles + w + v; the output ring sits after the stages).  A remote
-// bulk store releases its shared-memory source only about one NVLink round trip after it
-// was issued (measured, r5d: one store in flight per CTA = 5 GB/s), so both rings keep
-// several stores in flight.
-__host__ __device__ constexpr int bulk_owner_tile(int N) { return N <= 4 ? 8192 : 4096; }
+// Owner tiles: bytes per input stream per tile, and the pipeline depth for N ranks.  A
+// stage holds one tile of every input stream (N partials, w, v); the updated w and v are
+// written back into the stage's own w / v tiles and leave by TMA bulk stores (local w, local
+// v, every peer's w), so the loop issues no generic global stores (a proxy fence behind them
+// waits for their completion: ~1 us per tile, r5g).  A stage is reloaded two tiles after its
+// stores were issued (a remote bulk store releases its source about one NVLink round trip
+// later), so SO-2 tiles of loads are in flight.
+__host__ __device__ constexpr int bulk_owner_tile(int N) { return N <= 3 ? 8192 : 4096; }
 __host__ __device__ constexpr int bulk_owner_stages(int N) {
-  return (kBulkRing - kOwnOut * bulk_owner_tile(N)) / ((N + 2) * bulk_owner_tile(N)) < kOwnBars
-             ? (kBulkRing - kOwnOut * bulk_owner_tile(N)) / ((N + 2) * bulk_owner_tile(N))
-             : kOwnBars;
+  return kBulkRing / ((N + 2) * bulk_owner_tile(N)) < kOwnBars ? kBulkRing / ((N + 2) * bulk_owner_tile(N))
+                                                                : kOwnBars;
 }
 
 __device__ __forceinline__ void tma_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
@@ -604,13 +604,12 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
   constexpr int SO = bulk_owner_stages(N);
   constexpr int TB = bulk_owner_tile(N);          // bytes per owner input stream per tile
   constexpr uint64_t TO = TB / sizeof(T);         // elements per owner tile
-  static_assert(SO >= 2, "owner pipeline needs two stages");
+  static_assert(SO >= 3, "owner pipeline needs three stages");
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
   extern __shared__ __align__(128) uint8_t ring[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kBulkRing);  // [S push][kOwnBars owner]
   uint64_t* obars = bars + S;
-  T* outt = reinterpret_cast<T*>(ring + (size_t)SO * (N + 2) * TB);  // kOwnOut output tiles
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
   if (threadIdx.x == 0) {
@@ -704,34 +703,37 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         if (upd) tma_load(st + N * TO, wme + t0, body, bar);
         if (fast) tma_load(st + (N + 1) * TO, a.v + t0, body, bar);
       };
+      constexpr int AHEAD = SO - 2;  // tiles of loads in flight
       if (threadIdx.x == 0)
-        for (uint32_t i = 0; i < min(ntile, (uint32_t)(SO - 1)); ++i) issue(i);
+        for (uint32_t i = 0; i < min(ntile, (uint32_t)AHEAD); ++i) issue(i);
       unsigned long long t_in = 0, t_iss = 0, t_comp = 0, t_st = 0, t_x = 0;
       const bool tr = a.trace && threadIdx.x == 0;
       for (uint32_t i = 0; i < ntile; ++i) {
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && i + AHEAD < ntile) {
           if (tr) t_x = globaltimer_ns();
-          if (i + SO - 1 < ntile) issue(i + SO - 1);  // slot of tile i-1, consumed
-          if (N > 1 && i >= (uint32_t)kOwnOut) tma_wait_read<kOwnOut - 1>();  // tile i-kOwnOut's sources read
+          // slot (i+AHEAD)%SO held tile i-2, whose stores were committed before tile i-1's
+          if (i >= 2) tma_wait_read_1();
+          issue(i + AHEAD);
           if (tr) t_iss += globaltimer_ns() - t_x;
         }
         const uint32_t g = gown + i;
         if (tr) t_x = globaltimer_ns();
         mbar_wait(&obars[g % SO], (g / SO) & 1u);
-        __syncthreads();  // output slot i % kOwnOut is free
         if (tr) t_in += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
         const uint64_t nfull = ((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W;  // vectors loaded by TMA
         const uint64_t nvec = (t1 - t0 + W - 1) / W;
-        const T* st = stage(i);
+        T* st = stage(i);
         const bool og = own_tile_src<T>(a.g, t0, t1) != nullptr;
-        T* out = outt + (i % kOwnOut) * TO;
+        T* wout = st + N * TO;                                   // updated w, in place
+        float* vout = reinterpret_cast<float*>(st + (N + 1) * TO);  // updated v, in place
         for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
           const uint64_t e = t0 + q * W;
           const int cnt = (int)min((uint64_t)W, t1 - e);
           T vals[N][W], w[W];
           float vv[W];
-          if (q < nfull) {
+          const bool in_smem = q < nfull;
+          if (in_smem) {
 #pragma unroll
             for (int s = 0; s < N; ++s) {
               if (s == me && !og)
@@ -739,8 +741,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
               else
                 memcpy(vals[s], st + s * TO + q * W, sizeof(vals[s]));
             }
-            if (upd) memcpy(w, st + N * TO + q * W, sizeof(w));
-            if (fast) memcpy(vv, reinterpret_cast<const float*>(st + (N + 1) * TO) + q * W, sizeof(vv));
+            if (upd) memcpy(w, wout + q * W, sizeof(w));
+            if (fast) memcpy(vv, vout + q * W, sizeof(vv));
           } else {  // ragged end of the layer (< 16 bytes): straight from global memory
 #pragma unroll
             for (int s = 0; s < N; ++s) {
@@ -768,30 +770,37 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
               gsum = tree_sum<N>(col, AddF32{});
             w[k] = apply_update<T>(w[k], gsum, vv[k], a);
           }
-          st_vec<T>(wme + e, cnt, w);
-          if (fast) st_vec<float>(a.v + e, cnt, vv);
-          st_vec<T>(out + q * W, cnt, w);
+          st_vec<T>(wout + q * W, cnt, w);  // all-gather / local store source (smem)
+          if (fast) st_vec<float>(vout + q * W, cnt, vv);
+          if (!in_smem) {  // the ragged vector is not covered by the bulk stores
+            st_vec<T>(wme + e, cnt, w);
+            if (fast) st_vec<float>(a.v + e, cnt, vv);
+          }
         }
         // every writer orders its generic smem writes before the async proxy's reads
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (tr) t_comp += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         if (threadIdx.x == 0) {
-          if (N > 1) {
-            const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
-            if (body) {
-              for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, out, (uint32_t)body);
-              tma_commit();
-            }
-            for (int d = 1; d < N; ++d) {  // ragged end of the layer (< 16 bytes)
-              uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
-              for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(out)[b];
-            }
+          const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
+          if (body) {
+            tma_store(wme + t0, wout, (uint32_t)body);
+            if (fast) tma_store(a.v + t0, vout, (uint32_t)(body / sizeof(T) * sizeof(float)));
+            for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, wout, (uint32_t)body);
+          }
+          tma_commit();  // one group per tile (possibly empty): the ring accounting above counts tiles
+          for (int d = 1; d < N; ++d) {  // ragged end of the layer (< 16 bytes)
+            uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
+            for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(wout)[b];
           }
           if (tr) t_st += globaltimer_ns() - t_x;
         }
       }
       gown += ntile;
+      if (threadIdx.x == 0) {  // every tile's bulk stores done (also the local w / v)
+        tma_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       if (tr) {
         a.trace[(uint64_t)it * 8 + 4] = t_in;    // input tiles + barrier
         a.trace[(uint64_t)it * 8 + 5] = t_iss;   // issuing the loads (+ output-ring wait)
@@ -799,8 +808,6 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         a.trace[(uint64_t)it * 8 + 7] = t_st;    // issuing the all-gather stores
       }
       if (N > 1 && threadIdx.x == 0) {
-        tma_wait_all();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
         fence_acq_rel_sys();
         for (int d = 1; d < N; ++d) red_release_sys_add(a.mflags[(me + d) % N] + a.layer, 1u);
       }
