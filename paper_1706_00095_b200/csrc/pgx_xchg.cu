@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       constexpr int AHEAD = SO - 2;  // tiles of loads in flight
       if (threadIdx.x == 0)
         for (uint32_t i = 0; i < min(ntile, (uint32_t)AHEAD); ++i) issue(i);
-      unsigned long long t_in = 0, t_iss = 0, t_comp = 0, t_st = 0, t_x = 0;
+      unsigned long long t_in = 0, t_iss = 0, t_comp = 0, t_st = 0, t_x = 0, t_fence = 0, t_bar = 0;
       const bool tr = a.trace && threadIdx.x == 0;
       for (uint32_t i = 0; i < ntile; ++i) {
         if (threadIdx.x == 0 && i + AHEAD < ntile) {
@@ -777,10 +777,17 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
             if (fast) st_vec<float>(a.v + e, cnt, vv);
           }
         }
-        // every writer orders its generic smem writes before the async proxy's reads
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
         if (tr) t_comp += globaltimer_ns() - t_x, t_x = globaltimer_ns();
+        // every writer orders its generic smem writes before the async proxy's reads
+#ifndef PGX_BULK_FENCE_T0
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+        if (tr) t_fence += globaltimer_ns() - t_x, t_x = globaltimer_ns();
+        __syncthreads();
+#ifdef PGX_BULK_FENCE_T0
+        if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+        if (tr) t_bar += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         if (threadIdx.x == 0) {
           const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
           if (body) {
@@ -802,10 +809,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       if (tr) {
-        a.trace[(uint64_t)it * 8 + 4] = t_in;    // input tiles + barrier
-        a.trace[(uint64_t)it * 8 + 5] = t_iss;   // issuing the loads (+ output-ring wait)
-        a.trace[(uint64_t)it * 8 + 6] = t_comp;  // fold + update + barrier
-        a.trace[(uint64_t)it * 8 + 7] = t_st;    // issuing the all-gather stores
+        a.trace[(uint64_t)it * 8 + 3] = t_fence;  // (overrides the SM id) proxy fence
+        a.trace[(uint64_t)it * 8 + 4] = t_in;     // input tiles
+        a.trace[(uint64_t)it * 8 + 5] = t_iss;    // ring wait + issuing the loads
+        a.trace[(uint64_t)it * 8 + 6] = t_comp * 1000000ull + t_bar;  // fold+update | barrier
+        a.trace[(uint64_t)it * 8 + 7] = t_st;     // issuing the stores
       }
       if (N > 1 && threadIdx.x == 0) {
         fence_acq_rel_sys();
