@@ -597,7 +597,26 @@ __device__ __forceinline__ const T* own_tile_src(const Pieces& P, uint64_t t0, u
   return nullptr;
 }
 
-template <int N, class T>
+// The fused update with the mode fixed at compile time (same per-element expressions as
+// apply_update): the bulk kernel runs on few SMs, so its fold is issue-bound and every
+// instruction per element counts.
+template <int MODE, class T>
+__device__ __forceinline__ T bulk_update(T w, T g, float& v, double lr, float scale, float mu, float wd) {
+  if constexpr (MODE == PGX_MODE_REF64) {
+    return __dsub_rn(w, __dmul_rn(lr, g));
+  } else if constexpr (MODE == PGX_MODE_REF32) {
+    return __double2float_rn(__dsub_rn((double)w, __dmul_rn(lr, (double)g)));
+  } else if constexpr (MODE == PGX_MODE_SUM32) {
+    return __fmul_rn(scale, g);
+  } else {
+    const float gg = __fadd_rn(__fmul_rn(scale, g), __fmul_rn(wd, w));
+    const float vv = __fadd_rn(__fmul_rn(mu, v), __fmul_rn((float)lr, gg));
+    v = vv;
+    return __fsub_rn(w, vv);
+  }
+}
+
+template <int N, class T, int MODE>
 __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
   constexpr int W = VecT<T>::W;
   constexpr int S = kBulkStages;
@@ -619,8 +638,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
   __syncthreads();
   uint32_t gload = 0, gown = 0;  // push / owner load counters (mbarrier phases; every thread tracks gown)
   const int me = a.rank;
-  const bool fast = sizeof(T) == 4 && a.mode == PGX_MODE_FAST32;
-  const bool upd = a.mode != PGX_MODE_SUM32;
+  constexpr bool fast = MODE == PGX_MODE_FAST32;
+  constexpr bool upd = MODE != PGX_MODE_SUM32;
+  const double lr = a.lr;
+  const float scale = a.scale, mu = a.mu, wd = a.wd;
   while (true) {
     const uint32_t it = claim(a.queue, &s_item) + a.item_begin;
     if (it >= a.item_end) break;
@@ -721,42 +742,33 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         mbar_wait(&obars[g % SO], (g / SO) & 1u);
         if (tr) t_in += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
-        const uint64_t nfull = ((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W;  // vectors loaded by TMA
-        const uint64_t nvec = (t1 - t0 + W - 1) / W;
+        using V = typename VecT<T>::V;
+        const uint32_t nfull = (uint32_t)(((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W);  // TMA-loaded vectors
+        const uint32_t nvec = (uint32_t)((t1 - t0 + W - 1) / W);
         T* st = stage(i);
         const bool og = own_tile_src<T>(a.g, t0, t1) != nullptr;
-        T* wout = st + N * TO;                                   // updated w, in place
+        T* wout = st + N * TO;                                      // updated w, in place
         float* vout = reinterpret_cast<float*>(st + (N + 1) * TO);  // updated v, in place
-        for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
-          const uint64_t e = t0 + q * W;
-          const int cnt = (int)min((uint64_t)W, t1 - e);
+        const V* sv = reinterpret_cast<const V*>(st);
+        for (uint32_t q = threadIdx.x; q < nfull; q += blockDim.x) {  // full vectors: shared memory only
           T vals[N][W], w[W];
           float vv[W];
-          const bool in_smem = q < nfull;
-          if (in_smem) {
 #pragma unroll
-            for (int s = 0; s < N; ++s) {
-              if (s == me && !og)
-                grad_vec<T>(a.g, e, cnt, vals[s]);
-              else
-                memcpy(vals[s], st + s * TO + q * W, sizeof(vals[s]));
+          for (int s = 0; s < N; ++s) {
+            if (s == me && !og) {  // own gradient not TMA-loadable (piece edge / misaligned): global
+              grad_vec<T>(a.g, t0 + (uint64_t)q * W, W, vals[s]);
+            } else {
+              const V x = sv[s * (TO / W) + q];
+              memcpy(vals[s], &x, sizeof(x));
             }
-            if (upd) memcpy(w, wout + q * W, sizeof(w));
-            if (fast) memcpy(vv, vout + q * W, sizeof(vv));
-          } else {  // ragged end of the layer (< 16 bytes): straight from global memory
-#pragma unroll
-            for (int s = 0; s < N; ++s) {
-              if (s == me)
-                grad_vec<T>(a.g, e, cnt, vals[s]);
-              else
-                ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt, vals[s]);
-            }
-            if (upd) ld_vec<T>(wme + e, cnt, w);
-            if (fast) ld_vec<float>(a.v + e, cnt, vv);
           }
-          if (!upd) {
-#pragma unroll
-            for (int k = 0; k < W; ++k) w[k] = T(0);
+          if constexpr (upd) {
+            const V x = sv[N * (TO / W) + q];
+            memcpy(w, &x, sizeof(x));
+          }
+          if constexpr (fast) {
+            const float4 x = reinterpret_cast<const float4*>(vout)[q];
+            memcpy(vv, &x, sizeof(x));
           }
 #pragma unroll
           for (int k = 0; k < W; ++k) {
@@ -768,14 +780,42 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
               gsum = tree_sum<N>(col, AddF64{});
             else
               gsum = tree_sum<N>(col, AddF32{});
-            w[k] = apply_update<T>(w[k], gsum, vv[k], a);
+            w[k] = bulk_update<MODE, T>(upd ? w[k] : T(0), gsum, vv[k], lr, scale, mu, wd);
           }
-          st_vec<T>(wout + q * W, cnt, w);  // all-gather / local store source (smem)
-          if (fast) st_vec<float>(vout + q * W, cnt, vv);
-          if (!in_smem) {  // the ragged vector is not covered by the bulk stores
-            st_vec<T>(wme + e, cnt, w);
-            if (fast) st_vec<float>(a.v + e, cnt, vv);
+          V y;
+          memcpy(&y, w, sizeof(y));
+          reinterpret_cast<V*>(wout)[q] = y;
+          if constexpr (fast) {
+            float4 z;
+            memcpy(&z, vv, sizeof(z));
+            reinterpret_cast<float4*>(vout)[q] = z;
           }
+        }
+        if (nfull < nvec && threadIdx.x == 0) {  // the layer's ragged last vector (< 16 bytes): global memory
+          const uint64_t e = t0 + (uint64_t)nfull * W;
+          const int cnt = (int)(t1 - e);
+          T vals[N][W], w[W] = {};
+          float vv[W] = {};
+#pragma unroll
+          for (int s = 0; s < N; ++s) {
+            if (s == me)
+              grad_vec<T>(a.g, e, cnt, vals[s]);
+            else
+              ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt, vals[s]);
+          }
+          if (upd) ld_vec<T>(wme + e, cnt, w);
+          if (fast) ld_vec<float>(a.v + e, cnt, vv);
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            T col[N];
+#pragma unroll
+            for (int s = 0; s < N; ++s) col[s] = vals[s][k];
+            const T gsum = sizeof(T) == 8 ? (T)tree_sum<N>(col, AddF64{}) : (T)tree_sum<N>(col, AddF32{});
+            w[k] = bulk_update<MODE, T>(w[k], gsum, vv[k], lr, scale, mu, wd);
+          }
+          st_vec<T>(wout + (uint64_t)nfull * W, cnt, w);  // source of the peers' ragged bytes
+          st_vec<T>(wme + e, cnt, w);
+          if (fast) st_vec<float>(a.v + e, cnt, vv);
         }
         if (tr) t_comp += globaltimer_ns() - t_x, t_x = globaltimer_ns();
         // every writer orders its generic smem writes before the async proxy's reads
@@ -1641,19 +1681,30 @@ void launch_twoshot(int N, bool tma, int want, int dev, cudaStream_t s, const XA
   }
 }
 
-template <class T>
+template <int N, class T, int MODE>
+void launch_bulk_nm(int grid, int dev, cudaStream_t s, const XArgs& a) {
+  static bool attr[64] = {};  // per device
+  if (!attr[dev & 63]) {
+    cudaFuncSetAttribute(k_twoshot_bulk<N, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+    attr[dev & 63] = true;
+  }
+  k_twoshot_bulk<N, T, MODE><<<grid, kBulkThreads, kBulkSmem, s>>>(a);
+}
+
+template <int N>
+void launch_bulk_n(int grid, int dev, cudaStream_t s, const XArgs& a) {
+  switch (a.mode) {
+    case PGX_MODE_REF64: launch_bulk_nm<N, double, PGX_MODE_REF64>(grid, dev, s, a); break;
+    case PGX_MODE_REF32: launch_bulk_nm<N, float, PGX_MODE_REF32>(grid, dev, s, a); break;
+    case PGX_MODE_SUM32: launch_bulk_nm<N, float, PGX_MODE_SUM32>(grid, dev, s, a); break;
+    default: launch_bulk_nm<N, float, PGX_MODE_FAST32>(grid, dev, s, a); break;
+  }
+}
+
 void launch_twoshot_bulk(int N, int grid, int dev, cudaStream_t s, const XArgs& a) {
   switch (N) {
-#define PGX_CASE(n)                                                                                      \
-  case n: {                                                                                              \
-    static bool attr[64] = {};                                                                           \
-    if (!attr[dev & 63]) {                                                                               \
-      cudaFuncSetAttribute(k_twoshot_bulk<n, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem); \
-      attr[dev & 63] = true;                                                                             \
-    }                                                                                                    \
-    k_twoshot_bulk<n, T><<<grid, kBulkThreads, kBulkSmem, s>>>(a);                                       \
-    break;                                                                                               \
-  }
+#define PGX_CASE(n) \
+  case n: launch_bulk_n<n>(grid, dev, s, a); break;
     PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
 #undef PGX_CASE
   }
@@ -2604,10 +2655,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     if (n) {
       ++x->launches;
       int grid = (int)std::min<uint32_t>(n, (uint32_t)P.grid);
-      if (x->esz == 8)
-        launch_twoshot_bulk<double>(x->world, grid, x->dev, s, a);
-      else
-        launch_twoshot_bulk<float>(x->world, grid, x->dev, s, a);
+      launch_twoshot_bulk(x->world, grid, x->dev, s, a);
     }
   } else if (P.variant == PGX_VARIANT_TWOSHOT) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
