@@ -724,7 +724,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         if (upd) tma_load(st + N * TO, wme + t0, body, bar);
         if (fast) tma_load(st + (N + 1) * TO, a.v + t0, body, bar);
       };
-      constexpr int AHEAD = SO - 2;  // tiles of loads in flight
+#ifndef PGX_BULK_LAG
+#define PGX_BULK_LAG 2
+#endif
+      constexpr int LAG = PGX_BULK_LAG;  // a stage is reloaded LAG tiles after its stores were issued
+      constexpr int AHEAD = SO - LAG;    // tiles of loads in flight
       if (threadIdx.x == 0)
         for (uint32_t i = 0; i < min(ntile, (uint32_t)AHEAD); ++i) issue(i);
       unsigned long long t_in = 0, t_iss = 0, t_comp = 0, t_st = 0, t_x = 0, t_fence = 0, t_bar = 0;
@@ -732,8 +736,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       for (uint32_t i = 0; i < ntile; ++i) {
         if (threadIdx.x == 0 && i + AHEAD < ntile) {
           if (tr) t_x = globaltimer_ns();
-          // slot (i+AHEAD)%SO held tile i-2, whose stores were committed before tile i-1's
-          if (i >= 2) tma_wait_read_1();
+          // slot (i+AHEAD)%SO held tile i-LAG; one store group per tile
+          if (i >= (uint32_t)LAG) tma_wait_read<LAG - 1>();
           issue(i + AHEAD);
           if (tr) t_iss += globaltimer_ns() - t_x;
         }
@@ -785,11 +789,20 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
           V y;
           memcpy(&y, w, sizeof(y));
           reinterpret_cast<V*>(wout)[q] = y;
+#ifdef PGX_BULK_STG
+          reinterpret_cast<V*>(wme + t0)[q] = y;  // local weights / momentum by the LSU
+          if constexpr (fast) {
+            float4 z;
+            memcpy(&z, vv, sizeof(z));
+            reinterpret_cast<float4*>(a.v + t0)[q] = z;
+          }
+#else
           if constexpr (fast) {
             float4 z;
             memcpy(&z, vv, sizeof(z));
             reinterpret_cast<float4*>(vout)[q] = z;
           }
+#endif
         }
         if (nfull < nvec && threadIdx.x == 0) {  // the layer's ragged last vector (< 16 bytes): global memory
           const uint64_t e = t0 + (uint64_t)nfull * W;
@@ -831,8 +844,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         if (threadIdx.x == 0) {
           const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
           if (body) {
+#ifndef PGX_BULK_STG
             tma_store(wme + t0, wout, (uint32_t)body);
             if (fast) tma_store(a.v + t0, vout, (uint32_t)(body / sizeof(T) * sizeof(float)));
+#endif
             for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, wout, (uint32_t)body);
           }
           tma_commit();  // one group per tile (possibly empty): the ring accounting above counts tiles
