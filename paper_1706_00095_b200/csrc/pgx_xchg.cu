@@ -499,27 +499,13 @@ __device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slo
 // and the elected thread bulk-stores each updated tile into every peer's weights.  16-24
 // CTAs saturate NVLink (tools/probe_push.cu: 689 GB/s push from 16 CTAs), so the layer
 // leaves the other SMs to the backward kernels it overlaps with.
-constexpr int kBulkThreads = 256;
+constexpr int kBulkThreads = 512;
 constexpr int kBulkStage = 32768;  // bytes per push ring slot
 constexpr int kBulkStages = 7;     // push ring: 224 KB
 constexpr int kBulkAhead = 3;      // push loads in flight; the other slots hold stores in flight
 constexpr int kBulkRing = kBulkStages * kBulkStage;
-constexpr int kOwnBars = 8;        // owner pipeline depth (max)
-constexpr size_t kBulkSmem = (size_t)kBulkRing + (kBulkStages + kOwnBars) * sizeof(uint64_t);
+constexpr size_t kBulkSmem = (size_t)kBulkRing + kBulkStages * sizeof(uint64_t);
 constexpr int kBulkCtas = 24;      // default grid of a bulk layer
-
-// Owner tiles: bytes per input stream per tile, and the pipeline depth for N ranks.  A
-// stage holds one tile of every input stream (N partials, w, v); the updated w and v are
-// written back into the stage's own w / v tiles and leave by TMA bulk stores (local w, local
-// v, every peer's w), so the loop issues no generic global stores (a proxy fence behind them
-// waits for their completion: ~1 us per tile, r5g).  A stage is reloaded two tiles after its
-// stores were issued (a remote bulk store releases its source about one NVLink round trip
-// later), so SO-2 tiles of loads are in flight.
-__host__ __device__ constexpr int bulk_owner_tile(int N) { return N <= 3 ? 8192 : 4096; }
-__host__ __device__ constexpr int bulk_owner_stages(int N) {
-  return kBulkRing / ((N + 2) * bulk_owner_tile(N)) < kOwnBars ? kBulkRing / ((N + 2) * bulk_owner_tile(N))
-                                                                : kOwnBars;
-}
 
 __device__ __forceinline__ void tma_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 template <int K>
@@ -582,21 +568,6 @@ __device__ __forceinline__ void bulk_stream(const BulkSeg* segs, int nseg, uint8
   gload += n;
 }
 
-// The own gradient's part of [t0, t1) as one 16-byte-aligned source inside one piece, or null.
-template <class T>
-__device__ __forceinline__ const T* own_tile_src(const Pieces& P, uint64_t t0, uint64_t t1) {
-  uint64_t pb = 0;
-  for (int k = 0; k < P.n; ++k) {
-    const uint64_t pe = P.end[k];
-    if (t0 >= pb && t1 <= pe) {
-      const T* p = static_cast<const T*>(P.p[k]) + (t0 - pb);
-      return (reinterpret_cast<uintptr_t>(p) & 15) ? nullptr : p;
-    }
-    pb = pe;
-  }
-  return nullptr;
-}
-
 // The fused update with the mode fixed at compile time (same per-element expressions as
 // apply_update): the bulk kernel runs on few SMs, so its fold is issue-bound and every
 // instruction per element counts.
@@ -620,23 +591,18 @@ template <int N, class T, int MODE>
 __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
   constexpr int W = VecT<T>::W;
   constexpr int S = kBulkStages;
-  constexpr int SO = bulk_owner_stages(N);
-  constexpr int TB = bulk_owner_tile(N);          // bytes per owner input stream per tile
-  constexpr uint64_t TO = TB / sizeof(T);         // elements per owner tile
-  static_assert(SO >= 3, "owner pipeline needs three stages");
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
   extern __shared__ __align__(128) uint8_t ring[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kBulkRing);  // [S push][kOwnBars owner]
-  uint64_t* obars = bars + S;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kBulkRing);  // push ring mbarriers
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
   if (threadIdx.x == 0) {
-    for (int k = 0; k < S + kOwnBars; ++k) mbar_init(&bars[k], 1);
+    for (int k = 0; k < S; ++k) mbar_init(&bars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t gload = 0, gown = 0;  // push / owner load counters (mbarrier phases; every thread tracks gown)
+  uint32_t gload = 0;  // thread 0's push load counter (mbarrier phases)
   const int me = a.rank;
   constexpr bool fast = MODE == PGX_MODE_FAST32;
   constexpr bool upd = MODE != PGX_MODE_SUM32;
@@ -688,8 +654,10 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       }
       trace_stamp(a, it, 2);
     } else {
-      // ---- owner slab: TMA-fed fold of the N contributions in tree order, fused update,
-      // bulk all-gather.  Thread 0 keeps SO-1 tiles of every input stream in flight.
+      // ---- owner slab: fold the N contributions in tree order + fused update with the LSU
+      // (local HBM streams, U vectors per thread, every load of a round in flight at once),
+      // the updated weights staged in a shared-memory ring and all-gathered into every
+      // peer's weights by TMA bulk stores (several rounds of stores in flight).
       const uint32_t c = it - a.push_items;
       const uint64_t lo = me * a.sl + (uint64_t)c * a.CH;
       const uint64_t hi = min(min(lo + a.CH, (uint64_t)(me + 1) * a.sl), a.S);
@@ -703,176 +671,90 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       trace_stamp(a, it, 1);
       const T* rx0 = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl - (uint64_t)me * a.sl;
       T* wme = static_cast<T*>(a.model[me]);
-      const uint32_t ntile = (uint32_t)((hi - lo + TO - 1) / TO);
-      auto stage = [&](uint32_t i) { return reinterpret_cast<T*>(ring + (size_t)((gown + i) % SO) * (N + 2) * TB); };
-      auto issue = [&](uint32_t i) {  // thread 0: every input stream of tile i
-        const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
-        const uint32_t body = (uint32_t)(((t1 - t0) * sizeof(T)) & ~uint64_t(15));
-        const T* og = own_tile_src<T>(a.g, t0, t1);
-        uint64_t* bar = &obars[(gown + i) % SO];
-        const uint32_t tx = body * ((N - 1) + (og ? 1 : 0) + (upd ? 1 : 0) + (fast ? 1 : 0));
-        mbar_expect_tx(bar, tx);
-        if (!body) return;
-        T* st = stage(i);
-        for (int s = 0; s < N; ++s) {
-          if (s == me) {
-            if (og) tma_load(st + s * TO, og, body, bar);
-          } else {
-            tma_load(st + s * TO, rx0 + (uint64_t)s * a.sl + t0, body, bar);
-          }
-        }
-        if (upd) tma_load(st + N * TO, wme + t0, body, bar);
-        if (fast) tma_load(st + (N + 1) * TO, a.v + t0, body, bar);
-      };
-#ifndef PGX_BULK_LAG
-#define PGX_BULK_LAG 2
-#endif
-      constexpr int LAG = PGX_BULK_LAG;  // a stage is reloaded LAG tiles after its stores were issued
-      constexpr int AHEAD = SO - LAG;    // tiles of loads in flight
-      if (threadIdx.x == 0)
-        for (uint32_t i = 0; i < min(ntile, (uint32_t)AHEAD); ++i) issue(i);
-      unsigned long long t_in = 0, t_iss = 0, t_comp = 0, t_st = 0, t_x = 0, t_fence = 0, t_bar = 0;
+      constexpr int U = N <= 4 ? 4 : 2;                         // vectors per thread per round
+      const uint64_t RE = (uint64_t)blockDim.x * U * W;         // elements per round
+      const int K = (int)(kBulkRing / (RE * sizeof(T)));         // output ring slots
+      unsigned long long t_ld = 0, t_ring = 0, t_st = 0, t_x = 0;
       const bool tr = a.trace && threadIdx.x == 0;
-      for (uint32_t i = 0; i < ntile; ++i) {
-        if (threadIdx.x == 0 && i + AHEAD < ntile) {
-          if (tr) t_x = globaltimer_ns();
-          // slot (i+AHEAD)%SO held tile i-LAG; one store group per tile
-          if (i >= (uint32_t)LAG) tma_wait_read<LAG - 1>();
-          issue(i + AHEAD);
-          if (tr) t_iss += globaltimer_ns() - t_x;
-        }
-        const uint32_t g = gown + i;
+      uint32_t r = 0;
+      for (uint64_t t0 = lo; t0 < hi; t0 += RE, ++r) {
+        const uint64_t t1 = min(t0 + RE, hi);
+        T* slot = reinterpret_cast<T*>(ring + (size_t)(r % K) * RE * sizeof(T));
         if (tr) t_x = globaltimer_ns();
-        mbar_wait(&obars[g % SO], (g / SO) & 1u);
-        if (tr) t_in += globaltimer_ns() - t_x, t_x = globaltimer_ns();
-        const uint64_t t0 = lo + (uint64_t)i * TO, t1 = min(t0 + TO, hi);
-        using V = typename VecT<T>::V;
-        const uint32_t nfull = (uint32_t)(((t1 - t0) * sizeof(T) / 16) * 16 / sizeof(T) / W);  // TMA-loaded vectors
-        const uint32_t nvec = (uint32_t)((t1 - t0 + W - 1) / W);
-        T* st = stage(i);
-        const bool og = own_tile_src<T>(a.g, t0, t1) != nullptr;
-        T* wout = st + N * TO;                                      // updated w, in place
-        float* vout = reinterpret_cast<float*>(st + (N + 1) * TO);  // updated v, in place
-        const V* sv = reinterpret_cast<const V*>(st);
-        for (uint32_t q = threadIdx.x; q < nfull; q += blockDim.x) {  // full vectors: shared memory only
-          T vals[N][W], w[W];
-          float vv[W];
+        T vals[U][N][W], w[U][W];
+        float vv[U][W];
+        int cnt[U];
 #pragma unroll
-          for (int s = 0; s < N; ++s) {
-            if (s == me && !og) {  // own gradient not TMA-loadable (piece edge / misaligned): global
-              grad_vec<T>(a.g, t0 + (uint64_t)q * W, W, vals[s]);
-            } else {
-              const V x = sv[s * (TO / W) + q];
-              memcpy(vals[s], &x, sizeof(x));
+        for (int u = 0; u < U; ++u) {  // every load of the round first
+          const uint64_t e = t0 + ((uint64_t)u * blockDim.x + threadIdx.x) * W;
+          cnt[u] = e < t1 ? (int)min((uint64_t)W, t1 - e) : 0;
+          if (cnt[u] > 0) {
+#pragma unroll
+            for (int s = 0; s < N; ++s) {
+              if (s == me)
+                grad_vec<T>(a.g, e, cnt[u], vals[u][s]);
+              else
+                ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt[u], vals[u][s]);
             }
+            if constexpr (upd) ld_vec<T>(wme + e, cnt[u], w[u]);
+            if constexpr (fast) ld_vec<float>(a.v + e, cnt[u], vv[u]);
           }
-          if constexpr (upd) {
-            const V x = sv[N * (TO / W) + q];
-            memcpy(w, &x, sizeof(x));
-          }
-          if constexpr (fast) {
-            const float4 x = reinterpret_cast<const float4*>(vout)[q];
-            memcpy(vv, &x, sizeof(x));
-          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (cnt[u] <= 0) continue;
+          const uint64_t q = (uint64_t)u * blockDim.x + threadIdx.x;
 #pragma unroll
           for (int k = 0; k < W; ++k) {
             T col[N];
 #pragma unroll
-            for (int s = 0; s < N; ++s) col[s] = vals[s][k];
+            for (int s = 0; s < N; ++s) col[s] = vals[u][s][k];
             T gsum;
             if constexpr (sizeof(T) == 8)
               gsum = tree_sum<N>(col, AddF64{});
             else
               gsum = tree_sum<N>(col, AddF32{});
-            w[k] = bulk_update<MODE, T>(upd ? w[k] : T(0), gsum, vv[k], lr, scale, mu, wd);
+            w[u][k] = bulk_update<MODE, T>(upd ? w[u][k] : T(0), gsum, vv[u][k], lr, scale, mu, wd);
           }
-          V y;
-          memcpy(&y, w, sizeof(y));
-          reinterpret_cast<V*>(wout)[q] = y;
-#ifdef PGX_BULK_STG
-          reinterpret_cast<V*>(wme + t0)[q] = y;  // local weights / momentum by the LSU
-          if constexpr (fast) {
-            float4 z;
-            memcpy(&z, vv, sizeof(z));
-            reinterpret_cast<float4*>(a.v + t0)[q] = z;
-          }
-#else
-          if constexpr (fast) {
-            float4 z;
-            memcpy(&z, vv, sizeof(z));
-            reinterpret_cast<float4*>(vout)[q] = z;
-          }
-#endif
+          st_vec<T>(wme + t0 + q * W, cnt[u], w[u]);
+          if constexpr (fast) st_vec<float>(a.v + t0 + q * W, cnt[u], vv[u]);
+          if (N > 1) st_vec<T>(slot + q * W, cnt[u], w[u]);  // all-gather source
         }
-        if (nfull < nvec && threadIdx.x == 0) {  // the layer's ragged last vector (< 16 bytes): global memory
-          const uint64_t e = t0 + (uint64_t)nfull * W;
-          const int cnt = (int)(t1 - e);
-          T vals[N][W], w[W] = {};
-          float vv[W] = {};
-#pragma unroll
-          for (int s = 0; s < N; ++s) {
-            if (s == me)
-              grad_vec<T>(a.g, e, cnt, vals[s]);
-            else
-              ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt, vals[s]);
+        if (tr) t_ld += globaltimer_ns() - t_x;
+        if (N > 1) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            if (tr) t_x = globaltimer_ns();
+            const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
+            if (body)
+              for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, slot, (uint32_t)body);
+            tma_commit();  // one group per round (possibly empty)
+            for (int d = 1; d < N; ++d) {  // ragged end of the layer (< 16 bytes)
+              uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
+              for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(slot)[b];
+            }
+            if (tr) t_st += globaltimer_ns() - t_x, t_x = globaltimer_ns();
+            // the next round writes slot (r+1)%K, last read by round r+1-K's stores
+            if (K > 1) {
+              if (K >= 6) tma_wait_read<4>(); else tma_wait_read<0>();
+            }
+            if (tr) t_ring += globaltimer_ns() - t_x;
           }
-          if (upd) ld_vec<T>(wme + e, cnt, w);
-          if (fast) ld_vec<float>(a.v + e, cnt, vv);
-#pragma unroll
-          for (int k = 0; k < W; ++k) {
-            T col[N];
-#pragma unroll
-            for (int s = 0; s < N; ++s) col[s] = vals[s][k];
-            const T gsum = sizeof(T) == 8 ? (T)tree_sum<N>(col, AddF64{}) : (T)tree_sum<N>(col, AddF32{});
-            w[k] = bulk_update<MODE, T>(w[k], gsum, vv[k], lr, scale, mu, wd);
-          }
-          st_vec<T>(wout + (uint64_t)nfull * W, cnt, w);  // source of the peers' ragged bytes
-          st_vec<T>(wme + e, cnt, w);
-          if (fast) st_vec<float>(a.v + e, cnt, vv);
+          __syncthreads();
         }
-        if (tr) t_comp += globaltimer_ns() - t_x, t_x = globaltimer_ns();
-        // every writer orders its generic smem writes before the async proxy's reads
-#ifndef PGX_BULK_FENCE_T0
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-        if (tr) t_fence += globaltimer_ns() - t_x, t_x = globaltimer_ns();
-        __syncthreads();
-#ifdef PGX_BULK_FENCE_T0
-        if (threadIdx.x == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-        if (tr) t_bar += globaltimer_ns() - t_x, t_x = globaltimer_ns();
-        if (threadIdx.x == 0) {
-          const uint64_t bytes = (t1 - t0) * sizeof(T), body = bytes & ~uint64_t(15);
-          if (body) {
-#ifndef PGX_BULK_STG
-            tma_store(wme + t0, wout, (uint32_t)body);
-            if (fast) tma_store(a.v + t0, vout, (uint32_t)(body / sizeof(T) * sizeof(float)));
-#endif
-            for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + t0, wout, (uint32_t)body);
-          }
-          tma_commit();  // one group per tile (possibly empty): the ring accounting above counts tiles
-          for (int d = 1; d < N; ++d) {  // ragged end of the layer (< 16 bytes)
-            uint8_t* dst = reinterpret_cast<uint8_t*>(static_cast<T*>(a.model[(me + d) % N]) + t0);
-            for (uint64_t b = body; b < bytes; ++b) dst[b] = reinterpret_cast<const uint8_t*>(wout)[b];
-          }
-          if (tr) t_st += globaltimer_ns() - t_x;
-        }
-      }
-      gown += ntile;
-      if (threadIdx.x == 0) {  // every tile's bulk stores done (also the local w / v)
-        tma_wait_all();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
-      if (tr) {
-        a.trace[(uint64_t)it * 8 + 3] = t_fence;  // (overrides the SM id) proxy fence
-        a.trace[(uint64_t)it * 8 + 4] = t_in;     // input tiles
-        a.trace[(uint64_t)it * 8 + 5] = t_iss;    // ring wait + issuing the loads
-        a.trace[(uint64_t)it * 8 + 6] = t_comp * 1000000ull + t_bar;  // fold+update | barrier
-        a.trace[(uint64_t)it * 8 + 7] = t_st;     // issuing the stores
       }
       if (N > 1 && threadIdx.x == 0) {
+        tma_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         fence_acq_rel_sys();
         for (int d = 1; d < N; ++d) red_release_sys_add(a.mflags[(me + d) % N] + a.layer, 1u);
+      }
+      if (tr) {
+        a.trace[(uint64_t)it * 8 + 4] = t_ld;    // loads + fold + update + local stores
+        a.trace[(uint64_t)it * 8 + 5] = t_st;    // issuing the all-gather stores
+        a.trace[(uint64_t)it * 8 + 6] = t_ring;  // waiting for an output slot
+        a.trace[(uint64_t)it * 8 + 7] = r;       // rounds
       }
       trace_stamp(a, it, 2);
     }

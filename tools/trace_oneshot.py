@@ -83,10 +83,10 @@ def main():
                         "push_item_us_med": statistics.median(p[2] - p[0] for p in push) / 1e3,
                         "owner_fold_us_med": statistics.median(o[2] - o[1] for o in own) / 1e3,
                         "owner_acc_us_med": [statistics.median(r[k] for r in t[(world - 1) * C_:]) / 1e3
-                                             for k in (3, 4, 5, 7)],
-                        "owner_comp_bar_us_med": [statistics.median(r[6] // 1000000 for r in t[(world - 1) * C_:]) / 1e3,
-                                                  statistics.median(r[6] % 1000000 for r in t[(world - 1) * C_:]) / 1e3],
-                        "owner_acc": "fence, input wait, ring wait + load issue, store issue (us per item)"})
+                                             for k in (4, 5, 6)],
+                        "owner_rounds": statistics.median(r[7] for r in t[(world - 1) * C_:]),
+                        "owner_acc": "TWOSHOT_BULK: fold round (loads+update+local stores), store issue, "
+                                     "output-ring wait (us per item)"})
     allr = [None] * world
     dist.all_gather_object(allr, out)
     if rank == 0:
