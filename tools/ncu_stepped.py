@@ -1,12 +1,13 @@
-"""One layer's exchange for N ranks emulated on ONE GPU, phases launched in dependency order
-(push of every rank, then every owner), so each exchange kernel can be profiled by ncu
-without spinning on a peer (single-GPU hazard rule, tests/test_gpu_exchange.py).  The
-kernels under ncu are the product kernels with the production plan for that layer
-(variant, chunk, grid); "peer" stores land in this GPU's HBM, so DRAM bytes and
-instruction-level evidence are real while NVLink counters are not (tools/ncu_rank0.sh
-covers those on real peers).
+"""Exchanges for N ranks emulated on ONE GPU, phases launched in dependency order (push of
+every rank, then every owner), so each exchange kernel can be profiled by ncu or checked by
+compute-sanitizer without spinning on a peer (single-GPU hazard rule,
+tests/test_gpu_exchange.py).  The kernels are the product kernels with the production plan
+for the layer (variant, chunk, grid); "peer" stores land in this GPU's HBM, so DRAM bytes and
+instruction-level evidence are real while NVLink counters are not (tools/nvlink_counters.py
+reads those on real peers).  With --check every rank's weights are compared bit for bit with
+the oracle after every iteration.
 
-    python tools/ncu_stepped.py --world 4 --elems 37752832 --variant twoshot --iters 3
+    python tools/ncu_stepped.py --world 4 --elems 37752832 --variants twoshot,twoshot_bulk --iters 3
 """
 
 from __future__ import annotations
@@ -19,6 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
+    import numpy as np
     import torch
 
     from paper_1706_00095_b200 import _lib
@@ -27,38 +29,64 @@ def main():
 
     ap = argparse.ArgumentParser()
     ap.add_argument("--world", type=int, default=4)
-    ap.add_argument("--elems", type=int, default=37752832)  # AlexNet fc6
-    ap.add_argument("--variant", default="twoshot")
+    ap.add_argument("--elems", default="37752832")  # AlexNet fc6; comma-separated layer list
+    ap.add_argument("--variants", default="twoshot")
     ap.add_argument("--mode", default="fast32")
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--check", action="store_true")
     args = ap.parse_args()
     N = args.world
-    world = LocalWorld(N, inline=False)
-    trs = [world.transport(r) for r in range(N)]
-    xs = [DeviceExchange(tr, [args.elems], mode=args.mode, variant=args.variant, chunk_elems=16384, lr=0.01,
-                         momentum=0.9, weight_decay=5e-4, max_ctas=args.ctas,
-                         flags=("allow_l128",) if args.variant == "oneshot_l128" else ()) for tr in trs]
-    for x in xs:
-        x.connect()
-    g = [[torch.randn(args.elems - 4096, device="cuda") * 1e-3, torch.randn(4096, device="cuda") * 1e-3]
-         for _ in range(N)]
-    for k in range(args.iters):
-        for r in range(N):
-            xs[r].launch(0, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
+    elems = [int(e) for e in args.elems.split(",")]
+    for variant in args.variants.split(","):
+        world = LocalWorld(N, inline=False)
+        trs = [world.transport(r) for r in range(N)]
+        xs = [DeviceExchange(tr, elems, mode=args.mode, variant=variant, chunk_elems=16384, lr=0.01,
+                             momentum=0.9, weight_decay=5e-4, max_ctas=args.ctas,
+                             flags=("allow_l128",) if variant == "oneshot_l128" else ()) for tr in trs]
+        for x in xs:
+            x.connect()
+            x.model.zero_()
         torch.cuda.synchronize()
-        for r in range(N):
-            xs[r].launch(0, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_OWNER)
-            torch.cuda.synchronize()
-        for r in range(N):
-            xs[r].gate(0, k, stream=trs[r].stream)
-        torch.cuda.synchronize()
-    assert all(tr.device_status() == 0 for tr in trs)
-    print({"variant": args.variant, "world": N, "elems": args.elems, "plan": xs[0].layer_plan(0),
-           "bytes": xs[0].layer_bytes(0)})
-    for x in xs:
-        x.close()
-    world.close()
+        if args.check:
+            from oracle import pipesgd_oracle as O
+            w = [np.zeros(n, np.float32) for n in elems]
+            v = [np.zeros(n, np.float32) for n in elems]
+        for k in range(args.iters):
+            for l in reversed(range(len(elems))):
+                n = elems[l]
+                gh = [np.random.default_rng([r, l, k]).standard_normal(n, dtype=np.float32) * np.float32(1e-3)
+                      for r in range(N)]
+                cut = n - min(4096, max(1, n // 8))
+                g = [[torch.from_numpy(a[:cut]).cuda(), torch.from_numpy(a[cut:]).cuda()] for a in gh]
+                if variant == "tree":  # children (higher ranks) before parents, then back down
+                    for r in reversed(range(N)):
+                        xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
+                        torch.cuda.synchronize()
+                    for r in range(N):
+                        xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_DOWN)
+                        torch.cuda.synchronize()
+                else:
+                    for r in range(N):
+                        xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
+                    torch.cuda.synchronize()
+                    for r in range(N):
+                        xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_OWNER)
+                        torch.cuda.synchronize()
+                for r in range(N):
+                    xs[r].gate(l, k, stream=trs[r].stream)
+                torch.cuda.synchronize()
+                if args.check:
+                    w[l], v[l] = O.exchange_iteration(gh, w[l], 0.01, "fast32", state=v[l], scale=1.0 / N,
+                                                      momentum=0.9, weight_decay=5e-4)
+                    for r in range(N):
+                        assert xs[r].layer_views[l].cpu().numpy().tobytes() == w[l].tobytes(), (variant, k, l, r)
+        assert all(tr.device_status() == 0 for tr in trs)
+        print({"variant": variant, "world": N, "elems": elems, "plan": [xs[0].layer_plan(l) for l in range(len(elems))],
+               "bytes": [xs[0].layer_bytes(l) for l in range(len(elems))], "checked": args.check}, flush=True)
+        for x in xs:
+            x.close()
+        world.close()
 
 
 if __name__ == "__main__":
