@@ -13,12 +13,12 @@ run() {  # name variants regex skip count [elems]
   local name=$1 var=$2 rx=$3 sk=$4 cnt=$5 el=${6:-$FC6}
   local cmd="python tools/ncu_stepped.py --world 4 --elems $el --variants $var --iters 2"
   timeout 300 $cmd > $O/r5o_plain_$name.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$rx -s $sk -c $cnt \
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$rx" -s $sk -c $cnt \
       -o $O/r5o_ncu_$name $cmd > $O/r5o_ncu_$name.log 2>&1
   echo "ncu $name rc=$?"
 }
-run twoshot4 twoshot "k_twoshot<" 8 5
-run bulk4 twoshot_bulk "k_twoshot_bulk" 8 5
-run ce4 twoshot_ce "k_owner_local" 12 4
-run ll4 oneshot_ll "k_oneshot_ll" 8 5 65536
-run oneshot4 oneshot "k_oneshot<" 8 5 262144
+run twoshot4 twoshot "k_twoshot<4" 8 5
+run bulk4 twoshot_bulk "k_twoshot_bulk<4" 8 5
+run ce4 twoshot_ce "k_owner_local<4" 12 4
+run ll4 oneshot_ll "k_oneshot_ll<4" 8 5 65536
+run oneshot4 oneshot "k_oneshot<4" 8 5 262144
