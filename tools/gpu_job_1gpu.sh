@@ -19,6 +19,6 @@ run() {  # name variants regex skip count [elems]
 }
 run twoshot4 twoshot "k_twoshot<4" 8 5
 run bulk4 twoshot_bulk "k_twoshot_bulk<4" 8 5
-run ce4 twoshot_ce "k_owner_local<4" 12 4
+run ce4 twoshot_ce "k_owner_local<4" 16 4
 run ll4 oneshot_ll "k_oneshot_ll<4" 8 5 65536
 run oneshot4 oneshot "k_oneshot<4" 8 5 262144
