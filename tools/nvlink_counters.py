@@ -37,22 +37,30 @@ def nvml_handle(dev: int):
         return pynvml, pynvml.nvmlDeviceGetHandleByIndex(dev)
 
 
-FIELDS = ("DATA_TX", "DATA_RX", "RAW_TX", "RAW_RX")
+# (name, NVML field, unit bytes): per-link byte counters (COUNT_*, Blackwell) and the older
+# throughput counters (KiB); whichever the driver answers is used
+FIELDS = (("XMIT_BYTES", "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", 1), ("RCV_BYTES", "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", 1),
+          ("DATA_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX", 1024),
+          ("DATA_RX", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX", 1024),
+          ("RAW_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_TX", 1024), ("RAW_RX", "NVML_FI_DEV_NVLINK_THROUGHPUT_RAW_RX", 1024))
 
 
-def read_counters(nv, h) -> dict:
-    """KiB counters per field, summed over every link that answers."""
-    ids = {f: getattr(nv, "NVML_FI_DEV_NVLINK_THROUGHPUT_" + f) for f in FIELDS}
-    out = {f: 0 for f in FIELDS}
+def read_counters(nv, h) -> tuple[dict, dict]:
+    """Bytes per field summed over every link that answers, and the NVML return codes seen."""
+    out = {f: 0 for f, _, _ in FIELDS}
+    codes: dict = {}
     for link in range(18):
         try:
-            vals = nv.nvmlDeviceGetFieldValues(h, [(ids[f], link) for f in FIELDS])
-        except Exception:  # noqa: BLE001
+            vals = nv.nvmlDeviceGetFieldValues(h, [(getattr(nv, fid), link) for _, fid, _ in FIELDS])
+        except Exception as exc:  # noqa: BLE001
+            codes.setdefault("exception", repr(exc))
             continue
-        for f, v in zip(FIELDS, vals):
-            if getattr(v, "nvmlReturn", 1) == 0:
-                out[f] += int(v.value.ullVal)
-    return out
+        for (f, _, unit), v in zip(FIELDS, vals):
+            rc = int(getattr(v, "nvmlReturn", -1))
+            codes.setdefault(f, set()).add(rc)
+            if rc == 0:
+                out[f] += int(v.value.ullVal) * unit
+    return out, {k: sorted(v) if isinstance(v, set) else v for k, v in codes.items()}
 
 
 def main():
@@ -100,7 +108,7 @@ def main():
             one(k)
         torch.cuda.synchronize()
         tr.barrier()
-        c0 = read_counters(nv, h)
+        c0, codes = read_counters(nv, h)
         times = []
         for k in range(3, 3 + args.reps):
             tr.barrier_async(stream)
@@ -111,16 +119,16 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
         tr.barrier()
-        c1 = read_counters(nv, h)
-        per = {f: (c1[f] - c0[f]) * 1024 / args.reps for f in FIELDS}  # counters are KiB
+        c1, _ = read_counters(nv, h)
+        per = {f: (c1[f] - c0[f]) / args.reps for f, _, _ in FIELDS}
         ms = statistics.median(times)
         alg = 2 * (world - 1) / world * n * 4
         rec = {"variant": v, "rank": rank, "n_gpus": world, "bytes": n * 4, "ms_median": ms,
                "algorithmic_out_bytes": alg, "nvlink_bytes_per_exchange": per,
-               "tx_data_over_algorithmic": per["DATA_TX"] / alg if alg else None,
-               "achieved_tx_gbs": per["DATA_TX"] / (ms / 1e3) / 1e9,
+               "tx_over_algorithmic": (per["XMIT_BYTES"] or per["DATA_TX"]) / alg if alg else None,
+               "achieved_tx_gbs": (per["XMIT_BYTES"] or per["DATA_TX"]) / (ms / 1e3) / 1e9, "nvml_return_codes": codes,
                "achieved_busbw_gbs": alg / (ms / 1e3) / 1e9,
-               "counter_source": "NVML NVLINK_THROUGHPUT_{DATA,RAW}_{TX,RX}, summed over links",
+               "counter_source": "NVML NVLINK_COUNT_{XMIT,RCV}_BYTES and NVLINK_THROUGHPUT_*, summed over links",
                "note": "median event time includes the device barrier skew; counters cover every rep"}
         allr = [None] * world
         dist.all_gather_object(allr, rec)
