@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--large-chunk-elems", type=int, default=0, help="chunk of the large layers (0 = --chunk-elems)")
     p.add_argument("--low-priority-from", type=int, default=0,
                    help="layers with at least this many elements launch on a normal-priority stream (0 = off)")
+    p.add_argument("--xflags", default="", help="comma-separated exchange flags (exchange.FLAGS), e.g. bulk_lean")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager steps instead of a captured CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -267,7 +268,8 @@ def workload_config(world, args):
                   if args.workload == "alexnet" else "per-step working set (weights, grads, activations)",
             "chunk_elems": args.chunk_elems, "large_layers": {"variant": args.large, "ctas": args.large_ctas,
                                                                "chunk_elems": args.large_chunk_elems},
-            "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager"}
+            "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager",
+            "exchange_flags": args.xflags or None}
 
 
 # ------------------------------------------------------------------ model
@@ -404,7 +406,8 @@ def pgx_arm(args):
     xchg = DeviceExchange(tr, sizes, mode="fast32", variant=args.variant, chunk_elems=args.chunk_elems,
                           scale=1.0 / world, max_ctas=args.max_ctas,
                           low_priority_from=args.low_priority_from or None, large=args.large,
-                          large_ctas=args.large_ctas, large_chunk_elems=args.large_chunk_elems, **wl["hyper"])
+                          large_ctas=args.large_ctas, large_chunk_elems=args.large_chunk_elems,
+                          flags=tuple(f for f in args.xflags.split(",") if f), **wl["hyper"])
     gate = args.gate if args.gate != "auto" else ("model" if len(sizes) > 16 else "layer")
     bind = ModuleBinding(xchg, model.layers(), gate=gate)
     if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)

@@ -91,6 +91,7 @@ struct XArgs {
   uint32_t item_begin, item_end;       // claimed range (phase selection)
   uint64_t olo, ohi;                   // TWOSHOT_CE owner sub-range (ohi == 0: the whole shard)
   int single_buffer;                   // rx parity fixed at 0 (TWOSHOT_CEP: host-addressed copies)
+  int bulk_lean;                       // TWOSHOT_BULK: the lean footprint (PGX_XF_BULK_LEAN)
   unsigned long long* trace;           // debug: per-item globaltimer stamps (pgx_xchg_set_trace) or null
   const uint32_t* iter;                // device iteration counter (graph mode) or null
   double lr;
@@ -499,12 +500,18 @@ __device__ __forceinline__ void trace_stamp(const XArgs& a, uint32_t it, int slo
 // and the elected thread bulk-stores each updated tile into every peer's weights.  16-24
 // CTAs saturate NVLink (tools/probe_push.cu: 689 GB/s push from 16 CTAs), so the layer
 // leaves the other SMs to the backward kernels it overlaps with.
-constexpr int kBulkThreads = 512;
 constexpr int kBulkStage = 32768;  // bytes per push ring slot
-constexpr int kBulkStages = 7;     // push ring: 224 KB
-constexpr int kBulkAhead = 3;      // push loads in flight; the other slots hold stores in flight
-constexpr int kBulkRing = kBulkStages * kBulkStage;
-constexpr size_t kBulkSmem = (size_t)kBulkRing + kBulkStages * sizeof(uint64_t);
+// Two footprints: FULL owns an SM (512 threads, 224 KB ring: 3 loads + 4 stores in flight per
+// CTA); LEAN (256 threads, 64 KB ring: 1 load + 1 store in flight) leaves room on the SM for
+// the backward's CTAs, so the exchange is not starved of whole SMs while they run.
+template <bool LEAN>
+struct BulkGeo {
+  static constexpr int kThreads = LEAN ? 256 : 512;
+  static constexpr int kStages = LEAN ? 2 : 7;
+  static constexpr int kAhead = LEAN ? 1 : 3;
+  static constexpr int kRing = kStages * kBulkStage;
+  static constexpr size_t kSmem = (size_t)kRing + kStages * sizeof(uint64_t);
+};
 constexpr int kBulkCtas = 24;      // default grid of a bulk layer
 
 __device__ __forceinline__ void tma_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
@@ -532,13 +539,12 @@ __device__ __forceinline__ uint32_t bulk_tile(const BulkSeg* s, int n, uint32_t 
   return 0;
 }
 
-// One thread: copy the segments through the ring, kBulkAhead loads and up to
-// S - kBulkAhead stores in flight.  `gload` counts every load this CTA ever issued: load g
-// uses slot g % S at mbarrier phase (g / S) & 1.  Returns with stores possibly in flight
-// (caller: wait_group 0).
+// One thread: copy the segments through the ring, L loads and up to S - L stores in
+// flight.  `gload` counts every load this CTA ever issued: load g uses slot g % S at
+// mbarrier phase (g / S) & 1.  Returns with stores possibly in flight (caller: wait_group 0).
+template <int S, int L>
 __device__ __forceinline__ void bulk_stream(const BulkSeg* segs, int nseg, uint8_t* ring, uint64_t* bars,
                                             uint32_t& gload) {
-  constexpr int S = kBulkStages, L = kBulkAhead;
   uint32_t n = 0;
   for (int k = 0; k < nseg; ++k) n += (uint32_t)((segs[k].bytes + kBulkStage - 1) / kBulkStage);
   auto load = [&](uint32_t j) {
@@ -587,14 +593,29 @@ __device__ __forceinline__ T bulk_update(T w, T g, float& v, double lr, float sc
   }
 }
 
-template <int N, class T, int MODE>
-__global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
+// wait until at most k bulk groups are still reading their shared-memory sources
+__device__ __forceinline__ void tma_wait_read_n(int k) {
+  switch (k) {
+    case 0: tma_wait_read<0>(); break;
+    case 1: tma_wait_read<1>(); break;
+    case 2: tma_wait_read<2>(); break;
+    case 3: tma_wait_read<3>(); break;
+    case 4: tma_wait_read<4>(); break;
+    case 5: tma_wait_read<5>(); break;
+    case 6: tma_wait_read<6>(); break;
+    default: tma_wait_read<7>(); break;
+  }
+}
+
+template <int N, class T, int MODE, bool LEAN>
+__global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XArgs a) {
+  using G = BulkGeo<LEAN>;
   constexpr int W = VecT<T>::W;
-  constexpr int S = kBulkStages;
+  constexpr int S = G::kStages;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
   const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
   extern __shared__ __align__(128) uint8_t ring[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kBulkRing);  // push ring mbarriers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + G::kRing);  // push ring mbarriers
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
   if (threadIdx.x == 0) {
@@ -643,7 +664,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
         }
         pb = pe;
       }
-      if (threadIdx.x == 0 && nseg) bulk_stream(segs, nseg, ring, bars, gload);
+      if (threadIdx.x == 0 && nseg) bulk_stream<S, G::kAhead>(segs, nseg, ring, bars, gload);
       trace_stamp(a, it, 1);
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -673,7 +694,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
       T* wme = static_cast<T*>(a.model[me]);
       constexpr int U = N <= 4 ? 4 : 2;                         // vectors per thread per round
       const uint64_t RE = (uint64_t)blockDim.x * U * W;         // elements per round
-      const int K = (int)(kBulkRing / (RE * sizeof(T)));         // output ring slots
+      const int K = (int)(G::kRing / (RE * sizeof(T)));         // output ring slots
       unsigned long long t_ld = 0, t_ring = 0, t_st = 0, t_x = 0;
       const bool tr = a.trace && threadIdx.x == 0;
       uint32_t r = 0;
@@ -736,9 +757,7 @@ __global__ void __launch_bounds__(kBulkThreads, 1) k_twoshot_bulk(XArgs a) {
             }
             if (tr) t_st += globaltimer_ns() - t_x, t_x = globaltimer_ns();
             // the next round writes slot (r+1)%K, last read by round r+1-K's stores
-            if (K > 1) {
-              if (K >= 6) tma_wait_read<4>(); else tma_wait_read<0>();
-            }
+            tma_wait_read_n(K - 1);
             if (tr) t_ring += globaltimer_ns() - t_x;
           }
           __syncthreads();
@@ -1541,6 +1560,7 @@ XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
   a.st = world_status(x->w);
   a.iter = x->device_iter ? x->iter_dev : nullptr;
   a.trace = x->trace;
+  a.bulk_lean = (x->cfg.flags & PGX_XF_BULK_LEAN) != 0;
   return a;
 }
 
@@ -1578,14 +1598,23 @@ void launch_twoshot(int N, bool tma, int want, int dev, cudaStream_t s, const XA
   }
 }
 
-template <int N, class T, int MODE>
-void launch_bulk_nm(int grid, int dev, cudaStream_t s, const XArgs& a) {
+template <int N, class T, int MODE, bool LEAN>
+void launch_bulk_nml(int grid, int dev, cudaStream_t s, const XArgs& a) {
+  using G = BulkGeo<LEAN>;
   static bool attr[64] = {};  // per device
   if (!attr[dev & 63]) {
-    cudaFuncSetAttribute(k_twoshot_bulk<N, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBulkSmem);
+    cudaFuncSetAttribute(k_twoshot_bulk<N, T, MODE, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
     attr[dev & 63] = true;
   }
-  k_twoshot_bulk<N, T, MODE><<<grid, kBulkThreads, kBulkSmem, s>>>(a);
+  k_twoshot_bulk<N, T, MODE, LEAN><<<grid, G::kThreads, G::kSmem, s>>>(a);
+}
+
+template <int N, class T, int MODE>
+void launch_bulk_nm(int grid, int dev, cudaStream_t s, const XArgs& a) {
+  if (a.bulk_lean)
+    launch_bulk_nml<N, T, MODE, true>(grid, dev, s, a);
+  else
+    launch_bulk_nml<N, T, MODE, false>(grid, dev, s, a);
 }
 
 template <int N>
