@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=16384)
     ap.add_argument("--variants", default="twoshot,twoshot_ce,tree,nccl")
     ap.add_argument("--mode", default="fast32")
+    ap.add_argument("--xflags", default="", help="comma-separated exchange flags (exchange.FLAGS)")
     args = ap.parse_args()
 
     from paper_1706_00095_b200.exchange import DeviceExchange
@@ -66,7 +67,8 @@ def main():
                  "twoshot_bulk"):
             xs[v] = DeviceExchange(tr, elems, mode=args.mode, variant=v, chunk_elems=args.chunk, lr=0.01,
                                    momentum=0.9, weight_decay=5e-4, seg_base=seg, max_ctas=args.ctas,
-                                   flags=("allow_l128",) if v == "oneshot_l128" else ())
+                                   flags=tuple(f for f in args.xflags.split(",") if f)
+                                   + (("allow_l128",) if v == "oneshot_l128" else ()))
             seg += 2
     tr.barrier()
     for x in xs.values():
@@ -116,7 +118,7 @@ def main():
             rec = {"n_gpus": world, "variant": v, "bytes": nbytes, "ms": ms, "busbw_gbs": bus,
                    "frac_of_770": bus / 770.0 if bus else None, "ctas": args.ctas, "chunk_elems": args.chunk,
                    "update": ("fused " + args.mode) if v != "nccl" else "none (all-reduce only)",
-                   "hold_us": args.hold_us, "aligned_start": bool(args.align)}
+                   "hold_us": args.hold_us, "aligned_start": bool(args.align), "xflags": args.xflags or None}
             if rank == 0:
                 print(json.dumps(rec), flush=True)
             out.append(rec)
