@@ -1,16 +1,51 @@
 #!/bin/bash
 # The current GPU job (overwritten per gpurun call; the outputs land in gpurun_out/ and the
-# ones worth keeping are copied to profiles/).  r5p: N=4 in-step: CE vs bulk full / lean footprints.
+# ones worth keeping are copied to profiles/).  r5r (2 GPUs): ncu of the exchange kernels
+# stepped on one GPU (N=4 emulated, --set full) and across two GPUs (N=2, NVLink byte
+# counters), compute-sanitizer on the stepped exchanges, the 2-GPU multi/stress suite.
 cd "$(dirname "$0")/.." || exit 1
 O=gpurun_out
 mkdir -p $O
-TR="torchrun --nproc-per-node 4 --master-addr 127.0.0.1"
-timeout 300 $TR --master-port 29811 tools/sweep.py --min-kb 4096 --max-mb 256 --variants twoshot_bulk --ctas 48 > $O/r5p_sweep_n4_bulk48_full.jsonl 2> $O/r5p_sweep.err
-timeout 300 $TR --master-port 29817 tools/sweep.py --min-kb 4096 --max-mb 256 --variants twoshot_bulk --ctas 48 --xflags bulk_lean > $O/r5p_sweep_n4_bulk48_lean.jsonl 2>> $O/r5p_sweep.err
-timeout 300 $TR --master-port 29812 tools/nvlink_counters.py --mb 144 --variants twoshot,twoshot_ce,nccl --reps 20 > $O/r5p_nvlink_n4.jsonl 2> $O/r5p_nvlink.err
-B="bench.py --gpus 4 --steps 30 --warmup 5 --no-cpu-baseline"
-timeout 900 $TR --master-port 29813 $B > $O/r5p_bench4_ce.json 2> $O/r5p_bench4_ce.err
-timeout 900 $TR --master-port 29814 $B --large bulk --large-ctas 48 > $O/r5p_bench4_bulk48.json 2> $O/r5p_bench4_bulk48.err
-timeout 900 $TR --master-port 29815 $B --large bulk --large-ctas 48 --xflags bulk_lean > $O/r5p_bench4_bulk48_lean.json 2> $O/r5p_bench4_bulk48_lean.err
-timeout 900 $TR --master-port 29816 $B --large bulk --large-ctas 96 --xflags bulk_lean > $O/r5p_bench4_bulk96_lean.json 2> $O/r5p_bench4_bulk96_lean.err
+FC6=37752832
+
+# 1. ncu --set full, N=4 emulated on GPU 0 (each command first exits 0 without ncu)
+run() {  # name variants regex skip count [elems]
+  local name=$1 var=$2 rx=$3 sk=$4 cnt=$5 el=${6:-$FC6}
+  local cmd="python tools/ncu_stepped.py --world 4 --elems $el --variants $var --iters 2"
+  CUDA_VISIBLE_DEVICES=0 timeout 300 $cmd > $O/r5r_plain_$name.log 2>&1 && \
+  CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k regex:"$rx" -s $sk -c $cnt -o $O/r5r_ncu_$name $cmd > $O/r5r_ncu_$name.log 2>&1
+  echo "ncu $name rc=$?"
+}
+run twoshot4 twoshot "k_twoshot<.int.4," 8 5
+run bulk4 twoshot_bulk "k_twoshot_bulk<.int.4," 8 5
+run ce4 twoshot_ce "k_owner_local<.int.4," 16 4
+run ll4 oneshot_ll "k_oneshot_ll<.int.4>" 8 5 65536
+run oneshot4 oneshot "k_oneshot<.int.4," 8 5 262144
+run tree4 tree "k_tree_(up|down)<" 8 6
+
+# 2. NVLink bytes: N=2 stepped across GPUs 0 and 1 (push / owner phases never wait on a
+#    peer when launched in this order); ncu profiles device 0's launches only
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes_data_user.sum
+for v in twoshot twoshot_bulk oneshot tree; do
+  el=$FC6; [ $v = oneshot ] && el=262144
+  cmd="python tools/ncu_stepped.py --world 2 --devices 0,1 --elems $el --variants $v --iters 2 --check"
+  timeout 300 $cmd > $O/r5r_plain_nvl_$v.log 2>&1 && \
+  timeout 900 ncu --metrics $M --clock-control none --devices 0 --kernel-name-base demangled -k regex:"k_(twoshot|oneshot|tree)" \
+      --csv $cmd > $O/r5r_ncu_nvl_$v.csv 2> $O/r5r_ncu_nvl_$v.err
+  echo "nvl $v rc=$?"
+done
+
+# 3. compute-sanitizer on the stepped exchanges (small layers, every variant, checked vs oracle)
+SM="520,25050,400500,5010"
+for tool in memcheck racecheck synccheck; do
+  CUDA_VISIBLE_DEVICES=0 timeout 900 compute-sanitizer --tool $tool --kernel-name kns=pgx --print-limit 50 \
+      python tools/ncu_stepped.py --world 4 --elems $SM --variants twoshot,oneshot,oneshot_ll,twoshot_bulk,twoshot_ce,tree \
+      --iters 2 --check > $O/r5r_sanitizer_$tool.log 2>&1
+  echo "sanitizer $tool rc=$?"
+done
+
+# 4. the 2-GPU multi / stress suite with test ids in the log
+timeout 1200 python -m pytest tests/test_gpu_multi.py tests/test_gpu_stress.py -m gpu -rA -q > $O/r5r_pytest_multi_2gpus.log 2>&1
+echo "pytest rc=$?"
 echo done

@@ -35,11 +35,20 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--devices", default="", help="rank->GPU map, e.g. 0,1: peers' stores then cross NVLink")
     args = ap.parse_args()
     N = args.world
     elems = [int(e) for e in args.elems.split(",")]
+    devs = [int(d) for d in args.devices.split(",")] if args.devices else [0] * N
+    if len(devs) != N:
+        raise SystemExit("--devices needs one GPU per rank")
+
+    def sync():  # every GPU the ranks live on (torch.cuda.synchronize covers the current one only)
+        for d in sorted(set(devs)):
+            torch.cuda.synchronize(d)
+
     for variant in args.variants.split(","):
-        world = LocalWorld(N, inline=False)
+        world = LocalWorld(N, inline=False, devices=devs if args.devices else None)
         trs = [world.transport(r) for r in range(N)]
         xs = [DeviceExchange(tr, elems, mode=args.mode, variant=variant, chunk_elems=16384, lr=0.01,
                              momentum=0.9, weight_decay=5e-4, max_ctas=args.ctas,
@@ -47,7 +56,7 @@ def main():
         for x in xs:
             x.connect()
             x.model.zero_()
-        torch.cuda.synchronize()
+        sync()
         if args.check:
             from oracle import pipesgd_oracle as O
             w = [np.zeros(n, np.float32) for n in elems]
@@ -58,24 +67,25 @@ def main():
                 gh = [np.random.default_rng([r, l, k]).standard_normal(n, dtype=np.float32) * np.float32(1e-3)
                       for r in range(N)]
                 cut = n - min(4096, max(1, n // 8))
-                g = [[torch.from_numpy(a[:cut]).cuda(), torch.from_numpy(a[cut:]).cuda()] for a in gh]
+                g = [[torch.from_numpy(a[:cut]).to(f"cuda:{devs[r]}"), torch.from_numpy(a[cut:]).to(f"cuda:{devs[r]}")]
+                     for r, a in enumerate(gh)]
                 if variant == "tree":  # children (higher ranks) before parents, then back down
                     for r in reversed(range(N)):
                         xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
-                        torch.cuda.synchronize()
+                        sync()
                     for r in range(N):
                         xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_DOWN)
-                        torch.cuda.synchronize()
+                        sync()
                 else:
                     for r in range(N):
                         xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
-                    torch.cuda.synchronize()
+                    sync()
                     for r in range(N):
                         xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_OWNER)
-                        torch.cuda.synchronize()
+                        sync()
                 for r in range(N):
                     xs[r].gate(l, k, stream=trs[r].stream)
-                torch.cuda.synchronize()
+                sync()
                 if args.check:
                     w[l], v[l] = O.exchange_iteration(gh, w[l], 0.01, "fast32", state=v[l], scale=1.0 / N,
                                                       momentum=0.9, weight_decay=5e-4)
