@@ -205,11 +205,16 @@ enum pgx_variant {
                                  carried as an 8-byte {value, epoch} word (2x bytes)  */
   PGX_VARIANT_ONESHOT_L128 = 7,/* fp32 ONESHOT over 128-byte lines: 30 values + an 8-byte
                                  epoch flag per line, fence-free (128/120 bytes); needs
-                                 PGX_XF_ALLOW_L128 (probed, not architecturally promised) */
-  PGX_VARIANT_TWOSHOT_BULK = 8 /* TWOSHOT with every NVLink byte moved by TMA bulk copies
+                                 PGX_XF_ALLOW_L128 (the 128-byte write atomicity NCCL's
+                                 LL128 protocol also rests on; stress-tested, r5c)     */
+  PGX_VARIANT_TWOSHOT_BULK = 8,/* TWOSHOT with every NVLink byte moved by TMA bulk copies
                                  (cp.async.bulk through a shared-memory ring, one thread
                                  per CTA) on a capped grid, one system fence + flag per
                                  ~1 MB slab: the large-layer variant                     */
+  PGX_VARIANT_TWOSHOT_L128 = 9 /* fp32 TWOSHOT over the ONESHOT_L128 line format: shards
+                                 pushed as 128-byte lines to their owner, updated lines
+                                 gathered into every peer's staging area and installed
+                                 there; fence-free (mid-size layers); PGX_XF_ALLOW_L128  */
 };
 
 /* pgx_xchg_config.flags (ABI 3: these were process-environment knobs before) */
@@ -219,7 +224,7 @@ enum pgx_xchg_flag {
   PGX_XF_ONESHOT_SMALL_CHUNKS = 4, /* ONESHOT: ~one chunk per SM (measured slower, r3v)      */
   PGX_XF_AUTO_CHUNK_TREE = 8,      /* TREE: size-scaled chunks (measured slower, r3r)        */
   PGX_XF_NO_AUTO_CHUNK_NVLS = 16,  /* NVLS: keep chunk_elems instead of size-scaled chunks   */
-  PGX_XF_ALLOW_L128 = 32,          /* permit ONESHOT_L128 layers (sm_100 only)               */
+  PGX_XF_ALLOW_L128 = 32,          /* permit ONESHOT_L128 / TWOSHOT_L128 layers (sm_100 only) */
   PGX_XF_BULK_LEAN = 64            /* TWOSHOT_BULK: 256 threads + 64 KB ring per CTA (shares
                                       SMs with the backward) instead of 512 + 224 KB        */
 };

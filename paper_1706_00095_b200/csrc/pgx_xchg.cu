@@ -1004,6 +1004,7 @@ __global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_oneshot_l128(XArgs
         if (have)
           for (int i = 0; i < nv; ++i)
             if (e0 + i < a.S) w4[i] = __float_as_uint(grad_elem<float>(a.g, e0 + i));
+        __syncwarp();  // the 8 lanes of a line store together: one 128-byte write
         if (have) {
 #pragma unroll
           for (int d = 1; d < N; ++d) {
@@ -1069,6 +1070,213 @@ __global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_oneshot_l128(XArgs
           wp[e] = apply_update<float>(w, tree_sum<N>(col, AddF32{}), v, a);
           if (fast) a.v[e] = v;
         }
+      }
+    }
+  }
+  retire(a.queue);
+}
+
+// ============================================================== TWOSHOT_L128
+// TWOSHOT over 128-byte lines (the ONESHOT_L128 line format: 30 fp32 values + an 8-byte
+// {epoch, epoch} flag, one 16-byte volatile store per lane of an 8-lane group), for the
+// 1-16 MB range where a system fence + flag per chunk costs more than the bytes:
+//   push items    : line chunks of every peer's shard -> the owner's slot [parity][me]
+//   owner items   : poll the N-1 slots of my shard's lines, fold in tree order with my own
+//                   gradient, fused update into my weights (+ momentum), and the updated
+//                   line -> every peer's gather area [parity][line]
+//   install items : poll the gather area for another owner's lines -> my weights
+// Items are claimed push < owner < install, so a CTA only waits on items already claimed
+// by running CTAs (no deadlock at any residency).  No fence or flag round trip anywhere;
+// (N-1)/N of the layer crosses NVLink twice at 128/120 bytes per value byte.
+// Host-stepped launches: PHASE_PUSH, PHASE_OWNER, PHASE_DOWN (= install) in that order.
+
+// 2 or 4 consecutive gradient values at logical element e (e even): two 8-byte loads when
+// they sit in one piece at an 8-byte aligned address, else element by element.
+__device__ __forceinline__ void l128_grad(const Pieces& P, uint64_t e, int cnt, int nv, uint32_t* w4) {
+  int k = 0;
+  while (k < P.n - 1 && e >= P.end[k]) ++k;
+  const uint64_t base = k ? P.end[k - 1] : 0;
+  const float* src = static_cast<const float*>(P.p[k]) + (e - base);
+  if (cnt == nv && e + nv <= P.end[k] && (reinterpret_cast<uintptr_t>(src) & 7) == 0) {
+    const float2 x = __ldcs(reinterpret_cast<const float2*>(src));
+    w4[0] = __float_as_uint(x.x);
+    w4[1] = __float_as_uint(x.y);
+    if (nv == 4) {
+      const float2 y = __ldcs(reinterpret_cast<const float2*>(src + 2));
+      w4[2] = __float_as_uint(y.x);
+      w4[3] = __float_as_uint(y.y);
+    }
+  } else {
+    for (int i = 0; i < nv; ++i) w4[i] = i < cnt ? __float_as_uint(grad_elem<float>(P, e + i)) : 0u;
+  }
+}
+
+// 2 or 4 fp32 values at p (8-byte aligned) / back.
+__device__ __forceinline__ void l128_ld(const float* p, int cnt, int nv, float* out) {
+  if (cnt == nv) {
+    const float2 x = __ldcg(reinterpret_cast<const float2*>(p));
+    out[0] = x.x;
+    out[1] = x.y;
+    if (nv == 4) {
+      const float2 y = __ldcg(reinterpret_cast<const float2*>(p + 2));
+      out[2] = y.x;
+      out[3] = y.y;
+    }
+  } else {
+    for (int i = 0; i < 4; ++i) out[i] = i < cnt ? __ldcg(p + i) : 0.f;
+  }
+}
+__device__ __forceinline__ void l128_st(float* p, int cnt, int nv, const float* in) {
+  if (cnt == nv) {
+    *reinterpret_cast<float2*>(p) = make_float2(in[0], in[1]);
+    if (nv == 4) *reinterpret_cast<float2*>(p + 2) = make_float2(in[2], in[3]);
+  } else {
+    for (int i = 0; i < cnt; ++i) p[i] = in[i];
+  }
+}
+
+__device__ __forceinline__ void l128_put(uint8_t* p, const uint32_t* w4) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(w4[0]), "r"(w4[1]), "r"(w4[2]),
+               "r"(w4[3])
+               : "memory");
+}
+
+// Warp-collective: every 8-lane group polls its line (lane k's 16 bytes at p) until the
+// group's lane 7 sees {epoch, epoch}; returns false (warp-uniform) on timeout / abort.
+__device__ __forceinline__ bool l128_wait(const uint8_t* p, bool have, uint32_t epoch, int lane, uint32_t* x,
+                                          const Status& st) {
+  const int q = lane >> 3, k = lane & 7;
+  uint64_t t0 = 0;
+  for (uint32_t spins = 0;; ++spins) {
+    x[0] = x[1] = x[2] = x[3] = 0;
+    if (have)
+      asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3])
+                   : "l"(p)
+                   : "memory");
+    const unsigned ok = __ballot_sync(0xffffffffu, k == 7 && have && x[2] == epoch && x[3] == epoch);
+    const bool mine_ok = !have || ((ok >> (q * 8 + 7)) & 1u);
+    if (__all_sync(0xffffffffu, mine_ok)) return true;
+    if (spins > 1024) __nanosleep(32);
+    if ((spins & 1023) == 1023) {  // warp-uniform give-up decision (lane 0 decides)
+      int stop = 0;
+      if (lane == 0) {
+        if (!t0) t0 = globaltimer_ns();
+        stop = (st.word && *(volatile uint32_t*)st.word) || (st.timeout_ns && globaltimer_ns() - t0 > st.timeout_ns);
+        if (stop && st.word) atomicCAS(st.word, 0u, (uint32_t)PGX_E_TIMEOUT);
+      }
+      if (__shfl_sync(0xffffffffu, stop, 0)) return false;
+    }
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_twoshot_l128(XArgs a) {
+  const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
+  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  __shared__ uint32_t s_item;
+  const int me = a.rank;
+  const int lane = threadIdx.x & 31, q = lane >> 3, k = lane & 7;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint64_t lines = (a.S + kL128Vals - 1) / kL128Vals;
+  const uint64_t Ls = (lines + N - 1) / N;                  // lines per owner shard
+  const uint64_t agl = (lines * 32 + kAlignElems - 1) / kAlignElems * kAlignElems;
+  uint8_t* const rx_me = static_cast<uint8_t*>(a.rx[me]);
+  auto slot = [&](int r, int s) {  // rank r's reduce-scatter slot [parity][s] (Ls lines)
+    return static_cast<uint8_t*>(a.rx[r]) + ((uint64_t)parity * (N * a.sl + agl) + (uint64_t)s * a.sl) * 4;
+  };
+  auto gather = [&](int r) {  // rank r's gather area [parity] (every line of the layer)
+    return static_cast<uint8_t*>(a.rx[r]) + ((uint64_t)parity * (N * a.sl + agl) + (uint64_t)N * a.sl) * 4;
+  };
+  const int nv = k < 7 ? 4 : 2;  // values carried by this lane
+  constexpr int NP = N > 1 ? N - 1 : 1;
+  const uint32_t Cs = a.C, owner_end = a.push_items + Cs;
+  float* const wbase = static_cast<float*>(a.model[me]);
+  const bool fast = a.mode == PGX_MODE_FAST32;
+  while (true) {
+    const uint32_t it = claim(a.queue, &s_item) + a.item_begin;
+    if (it >= a.item_end) break;
+    int kind, j;  // 0 push (to owner j), 1 owner (j = me), 2 install (from owner j)
+    uint32_t c;
+    if (it < a.push_items) {
+      kind = 0;
+      c = it / NP;
+      j = (me + 1 + (int)(it % NP)) % N;
+    } else if (it < owner_end) {
+      kind = 1;
+      c = it - a.push_items;
+      j = me;
+    } else {
+      kind = 2;
+      const uint32_t i2 = it - owner_end;
+      c = i2 / NP;
+      j = (me + 1 + (int)(i2 % NP)) % N;
+    }
+    const uint64_t s_lo = (uint64_t)j * Ls, s_hi = min(s_lo + Ls, lines);
+    const uint64_t l_lo = s_lo + (uint64_t)c * a.CH, l_hi = min(l_lo + a.CH, s_hi);
+    bool failed = false;
+    for (uint64_t l0 = l_lo + (uint64_t)warp * 4; l0 < l_hi && !failed; l0 += (uint64_t)nwarps * 4) {
+      const uint64_t line = l0 + q;
+      const bool have = line < l_hi;
+      const uint64_t e0 = line * kL128Vals + 4 * k;
+      const int cnt = have && e0 < a.S ? (int)min((uint64_t)nv, a.S - e0) : 0;
+      if (kind == 0) {
+        uint32_t w4[4] = {0u, 0u, epoch, epoch};
+        if (cnt) l128_grad(a.g, e0, cnt, nv, w4);
+        __syncwarp();  // the 8 lanes of a line store together: one 128-byte write
+        if (have) l128_put(slot(j, me) + (line - s_lo) * 128 + 16 * k, w4);
+      } else if (kind == 1) {
+        float vals[N][4];
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          uint32_t x[4];
+          if (s == me) {
+            x[0] = x[1] = x[2] = x[3] = 0u;
+            if (cnt) l128_grad(a.g, e0, cnt, nv, x);
+          } else if (!l128_wait(slot(me, s) + (line - s_lo) * 128 + 16 * k, have, epoch, lane, x, a.st)) {
+            failed = true;
+            break;
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) vals[s][i] = __uint_as_float(x[i]);
+        }
+        if (failed) break;
+        float w[4] = {0.f, 0.f, 0.f, 0.f}, v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (cnt) {
+          if (a.mode != PGX_MODE_SUM32) l128_ld(wbase + e0, cnt, nv, w);
+          if (fast) l128_ld(a.v + e0, cnt, nv, v);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float col[N];
+#pragma unroll
+            for (int s = 0; s < N; ++s) col[s] = vals[s][i];
+            w[i] = apply_update<float>(w[i], tree_sum<N>(col, AddF32{}), v[i], a);
+          }
+          l128_st(wbase + e0, cnt, nv, w);
+          if (fast) l128_st(a.v + e0, cnt, nv, v);
+        }
+        uint32_t w4[4] = {__float_as_uint(w[0]), __float_as_uint(w[1]), epoch, epoch};
+        if (nv == 4) {
+          w4[2] = __float_as_uint(w[2]);
+          w4[3] = __float_as_uint(w[3]);
+        }
+        __syncwarp();
+        if (have) {
+#pragma unroll
+          for (int d = 1; d < N; ++d) l128_put(gather((me + d) % N) + line * 128 + 16 * k, w4);
+        }
+      } else {
+        uint32_t x[4];
+        if (!l128_wait(rx_me + ((uint64_t)parity * (N * a.sl + agl) + (uint64_t)N * a.sl) * 4 + line * 128 + 16 * k,
+                       have, epoch, lane, x, a.st)) {
+          failed = true;
+          break;
+        }
+        if (!cnt) continue;
+        float w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = __uint_as_float(x[i]);
+        l128_st(wbase + e0, cnt, nv, w);
       }
     }
   }
@@ -1692,6 +1900,28 @@ void launch_oneshot_l128(int N, int want, int dev, cudaStream_t s, const XArgs& 
   }
 }
 
+template <int N>
+int twoshot_l128_grid(int want, int dev) {
+  static int cap[PGX_MAX_RANKS] = {};
+  if (!cap[dev]) {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_twoshot_l128<N>, kThreads, 0);
+    cap[dev] = std::max(1, per_sm) * sm_count(dev);
+  }
+  return std::max(1, std::min(want, cap[dev]));
+}
+
+void launch_twoshot_l128(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n)                                                                \
+  case n:                                                                          \
+    k_twoshot_l128<n><<<twoshot_l128_grid<n>(want, dev), kThreads, 0, s>>>(a);     \
+    break;
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
 void launch_oneshot_ll(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
   switch (N) {
 #define PGX_CASE(n)                                                            \
@@ -2152,15 +2382,15 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   if (cfg->ce_rs_streams < 0 || cfg->ce_rs_streams > 2)
     return fail(PGX_E_CONFIG, "ce_rs_streams must be 0 (default), 1 or 2");
   for (int l = 0; l < cfg->num_layers; ++l) {
-    if (cfg->variant && cfg->variant[l] == PGX_VARIANT_ONESHOT_L128) {
+    if (cfg->variant && (cfg->variant[l] == PGX_VARIANT_ONESHOT_L128 || cfg->variant[l] == PGX_VARIANT_TWOSHOT_L128)) {
       // fence-free 128-byte lines rest on a probed (not promised) property of sm_100 NVLink
       // writes: only on explicit request, only on that architecture
       if (!(cfg->flags & PGX_XF_ALLOW_L128))
-        return fail(PGX_E_CONFIG, "layer %d: ONESHOT_L128 needs the PGX_XF_ALLOW_L128 opt-in flag", l);
+        return fail(PGX_E_CONFIG, "layer %d: the 128-byte-line variants need the PGX_XF_ALLOW_L128 opt-in flag", l);
       int dev = 0, major = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-      if (major != 10) return fail(PGX_E_CONFIG, "ONESHOT_L128 was validated on sm_100 only (device is sm_%d x)", major);
+      if (major != 10) return fail(PGX_E_CONFIG, "the 128-byte-line variants were validated on sm_100 only (device is sm_%d x)", major);
     }
   }
   pgx_xchg* x = new pgx_xchg();
@@ -2200,7 +2430,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     uint64_t CH = ch_given ? cfg->layer_chunk_elems[l] : cfg->chunk_elems;
     if (!ch_given && N > 1 && P.variant != PGX_VARIANT_TWOSHOT_CE && P.variant != PGX_VARIANT_ONESHOT &&
         P.variant != PGX_VARIANT_TWOSHOT_BULK &&
-        P.variant != PGX_VARIANT_ONESHOT_LL && P.variant != PGX_VARIANT_ONESHOT_L128 &&
+        P.variant != PGX_VARIANT_ONESHOT_LL && P.variant != PGX_VARIANT_ONESHOT_L128 && P.variant != PGX_VARIANT_TWOSHOT_L128 &&
         !(P.variant == PGX_VARIANT_TREE && !x->auto_chunk_tree) && !(P.variant == PGX_VARIANT_NVLS && !x->auto_chunk_nvls)) {
       // big shards: chunks of up to 64 K elements (~128 per shard) amortise the system fence
       // that ends every chunk; chunk_elems stays the minimum (profiles/r3e, r3n)
@@ -2300,6 +2530,39 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       P.nvlink_bytes = (uint64_t)(N - 1) * lines * 128;
       P.hbm_bytes = ((uint64_t)N + 2 + (cfg->mode == PGX_MODE_FAST32 ? 2 : cfg->mode == PGX_MODE_SUM32 ? -1 : 0)) * P.S * x->esz +
                     (uint64_t)(N - 1) * lines * 128;
+    } else if (P.variant == PGX_VARIANT_TWOSHOT_L128) {
+      if (x->esz != 4) {
+        delete x;
+        return fail(PGX_E_CONFIG, "layer %d: TWOSHOT_L128 carries fp32 values (not ref64)", l);
+      }
+      const uint64_t lines = (P.S + kL128Vals - 1) / kL128Vals;
+      const uint64_t Ls = (lines + N - 1) / N;
+      P.sl = align_up(Ls * 32, kAlignElems);            // reduce-scatter slot: Ls lines (4-byte units)
+      const uint64_t agl = align_up(lines * 32, kAlignElems);  // gather area: every line
+      // chunk = lines per item: ~one push item per SM, at least 64 lines (4 per warp)
+      CH = std::max<uint64_t>(64, ((uint64_t)std::max(N - 1, 1) * Ls + sms - 1) / sms);
+      if (ch_given) CH = std::max<uint64_t>(1, cfg->layer_chunk_elems[l] / kL128Vals);
+      P.CH = CH;
+      P.C = (uint32_t)((Ls + CH - 1) / CH);  // chunks per shard (ragged last shard: empty items)
+      P.K = N;
+      P.rx_off = rxoff;
+      rxoff = align_up(rxoff + 2 * ((uint64_t)N * P.sl + agl), kAlignElems);
+      P.rxflag_off = rxfoff;  // no flags: the epoch rides in every line
+      P.push_items = (uint32_t)(N - 1) * P.C;
+      P.down_items = (uint32_t)(N - 1) * P.C;  // install items (PGX_PHASE_DOWN)
+      P.items = P.push_items + P.C + P.down_items;
+      P.expected = 0;  // this rank's own install items complete the layer
+      P.grid = (int)std::min<uint64_t>(P.items, cap);
+      const uint64_t my_lines = std::min(lines, (uint64_t)(x->rank + 1) * Ls) - std::min(lines, (uint64_t)x->rank * Ls);
+      // out: my gradient's lines of the other shards + my updated lines to every peer
+      P.nvlink_bytes = N > 1 ? ((lines - my_lines) + (uint64_t)(N - 1) * my_lines) * 128 : 0;
+      const uint64_t own = std::min<uint64_t>(P.S, (uint64_t)(x->rank + 1) * Ls * kL128Vals) -
+                           std::min<uint64_t>(P.S, (uint64_t)x->rank * Ls * kL128Vals);
+      const uint64_t wv = cfg->mode == PGX_MODE_FAST32 ? 4 : cfg->mode == PGX_MODE_SUM32 ? 1 : 2;  // w (+v) traffic
+      // push reads + owner (own gradient, w/v) + rx lines written by peers and read back +
+      // gather lines written by owners and read back + install stores into the weights
+      P.hbm_bytes = 2 * (P.S - own) * x->esz + (1 + wv) * own * x->esz +
+                    2 * ((uint64_t)(N - 1) * my_lines + (lines - my_lines)) * 128;
     } else if (P.variant == PGX_VARIANT_ONESHOT_LL) {
       if (x->esz != 4) {
         delete x;
@@ -2531,6 +2794,23 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
         launch_oneshot_ll(x->world, want, x->dev, s, a);
       else
         launch_oneshot_l128(x->world, want, x->dev, s, a);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = xrecord(x->done[l], s);
+    if (prev != x->dev) cudaSetDevice(prev);
+    if (e != cudaSuccess) return fail(PGX_E_CUDA, "exchange launch failed: %s", cudaGetErrorString(e));
+    return PGX_OK;
+  }
+  if (P.variant == PGX_VARIANT_TWOSHOT_L128) {
+    // items: [0, push) reduce-scatter, [push, push + C) owner, [push + C, items) install
+    xrecord(x->ready[l], s);
+    const uint32_t own_end = P.push_items + P.C;
+    a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : (phases & PGX_PHASE_OWNER) ? P.push_items : own_end;
+    a.item_end = (phases & PGX_PHASE_DOWN) ? P.items : (phases & PGX_PHASE_OWNER) ? own_end : P.push_items;
+    if (a.item_end > a.item_begin) {
+      ++x->launches;
+      const int want = (int)std::min<uint32_t>(a.item_end - a.item_begin, (uint32_t)P.grid);
+      launch_twoshot_l128(x->world, want, x->dev, s, a);
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = xrecord(x->done[l], s);

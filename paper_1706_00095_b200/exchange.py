@@ -26,7 +26,7 @@ from .errors import ConfigError, ShapeError
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
             "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP,
             "oneshot_ll": _lib.VARIANT_ONESHOT_LL, "oneshot_l128": _lib.VARIANT_ONESHOT_L128,
-            "twoshot_bulk": _lib.VARIANT_TWOSHOT_BULK}
+            "twoshot_bulk": _lib.VARIANT_TWOSHOT_BULK, "twoshot_l128": _lib.VARIANT_TWOSHOT_L128}
 FLAGS = {"ce_rs_parts": _lib.XF_CE_RS_PARTS, "tma": _lib.XF_TMA, "oneshot_small_chunks": _lib.XF_ONESHOT_SMALL_CHUNKS,
          "auto_chunk_tree": _lib.XF_AUTO_CHUNK_TREE, "no_auto_chunk_nvls": _lib.XF_NO_AUTO_CHUNK_NVLS,
          "allow_l128": _lib.XF_ALLOW_L128, "bulk_lean": _lib.XF_BULK_LEAN}

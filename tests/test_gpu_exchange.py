@@ -24,7 +24,7 @@ def build(N, elems, mode, variant, chunk_elems=4096, **kw):
 
     world = LocalWorld(N, inline=False)
     trs = [world.transport(r) for r in range(N)]
-    if variant == "oneshot_l128":  # opt-in only (pgx.h PGX_XF_ALLOW_L128)
+    if variant in ("oneshot_l128", "twoshot_l128"):  # opt-in only (pgx.h PGX_XF_ALLOW_L128)
         kw.setdefault("flags", ("allow_l128",))
     xs = [DeviceExchange(tr, elems, mode=mode, variant=variant, chunk_elems=chunk_elems, **kw) for tr in trs]
     for x in xs:
@@ -44,6 +44,11 @@ def stepped_layer(xs, trs, l, k, pieces_by_rank, gate=True):
         sync()
         for r in range(N):
             xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=_lib.PHASE_OWNER)
+            sync()
+    elif xs[0].variants[l] == "twoshot_l128":  # push, owner (fold + update + gather), install
+        for ph in (_lib.PHASE_PUSH, _lib.PHASE_OWNER, _lib.PHASE_DOWN):
+            for r in range(N):
+                xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=ph)
             sync()
     else:
         for r in reversed(range(N)):  # children (higher ranks) before parents
@@ -68,10 +73,10 @@ def split_pieces(g, cut):
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128", "twoshot_bulk"])
+                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128"])
 @pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64", "sum32"])
 def test_exchange_matches_oracle(cuda, N, variant, mode):
-    if variant in ("oneshot_ll", "oneshot_l128") and mode == "ref64":
+    if variant in ("oneshot_ll", "oneshot_l128", "twoshot_l128") and mode == "ref64":
         pytest.skip("the LL one-shots carry fp32 values")
     elems = LENET if N in (2, 8) else CIFAR
     iters = 3
@@ -180,7 +185,8 @@ class _FixedGrad(torch.nn.Module):
         return (self.weight * self.c).sum() + (self.bias * self.d).sum()
 
 
-@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "twoshot_bulk"])
+@pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "twoshot_bulk",
+                                     "twoshot_l128"])
 @pytest.mark.parametrize("gate", ["layer", "model"])
 def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     """A captured training step (device iteration counter) applies exactly the oracle update."""
@@ -192,7 +198,7 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     world = LocalWorld(1, inline=False)
     tr = world.transport(0)
     x = DeviceExchange(tr, [40007], mode="fast32", variant=variant, lr=0.05, momentum=0.9, weight_decay=1e-3,
-                       flags=(("allow_l128",) if variant == "oneshot_l128" else ()))
+                       flags=(("allow_l128",) if "l128" in variant else ()))
     x.connect()
     w = torch.cat([m.weight.detach(), m.bias.detach()]).cpu().numpy()
     g = torch.cat([m.c, m.d]).cpu().numpy()
@@ -230,7 +236,7 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128", "twoshot_bulk"])
+                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128"])
 def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
     """Layers smaller than one vector per rank (empty owner shards), ragged tails and a
     piece boundary inside a vector, 8 ranks stepped on one GPU, ref32 bit-exact."""

@@ -35,7 +35,7 @@ def _exchange_worker(rank, world, port, variant, mode, late, q):
             tr.barrier()
         elems = LENET + [1 << 20]
         hyper = dict(lr=0.01, momentum=0.9, weight_decay=5e-4) if mode == "fast32" else dict(lr=0.05)
-        x = DeviceExchange(tr, elems, mode=mode, variant=variant, chunk_elems=16384, flags=(("allow_l128",) if variant == "oneshot_l128" else ()), **hyper)
+        x = DeviceExchange(tr, elems, mode=mode, variant=variant, chunk_elems=16384, flags=(("allow_l128",) if "l128" in variant else ()), **hyper)
         dt = np.float32
         w = [O.seeded_fill(42 ^ l, n, 1.0 / np.sqrt(n)).astype(dt) for l, n in enumerate(elems)]
         v = [np.zeros(n, np.float32) for n in elems]
@@ -109,7 +109,7 @@ def _ngpu():
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128",
-                                                                    "twoshot_bulk")
+                                                                    "twoshot_bulk", "twoshot_l128")
                                           for m in ("ref32", "fast32")]
                          + [("nvls", "fast32")])
 def test_concurrent_exchange_matches_oracle(variant, mode):
@@ -266,7 +266,7 @@ def _fault_worker(rank, world, port, variant, q):
     outcome = "no error"
     try:
         tr = DistTransport(rank, world, rank, timeout_s=2.0)
-        x = DeviceExchange(tr, [1 << 16], mode="fast32", variant=variant, flags=(("allow_l128",) if variant == "oneshot_l128" else ()), lr=0.01)
+        x = DeviceExchange(tr, [1 << 16], mode="fast32", variant=variant, flags=(("allow_l128",) if "l128" in variant else ()), lr=0.01)
         tr.barrier()
         x.connect()
         g = torch.ones(1 << 16, device="cuda")
@@ -290,7 +290,7 @@ def _fault_worker(rank, world, port, variant, q):
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot_ll", "oneshot_l128",
-                                     "twoshot_bulk"])
+                                     "twoshot_bulk", "twoshot_l128"])
 def test_dead_peer_surfaces_as_transport_error(variant):
     out = _spawn(_fault_worker, 2, variant)
     assert out[0][1].startswith("TransportError"), out
@@ -329,7 +329,7 @@ def _graph_worker(rank, world, port, variant, gate, use_graph, q):
         mods = [Fixed(n, rank) for n in sizes]
         layers = [(m, [m.weight, m.bias]) for m in mods]
         tr = DistTransport(rank, world, rank, timeout_s=20.0)
-        x = DeviceExchange(tr, [n + 7 for n in sizes], mode="fast32", variant=variant, flags=(("allow_l128",) if variant == "oneshot_l128" else ()), lr=0.05, momentum=0.9,
+        x = DeviceExchange(tr, [n + 7 for n in sizes], mode="fast32", variant=variant, flags=(("allow_l128",) if "l128" in variant else ()), lr=0.05, momentum=0.9,
                            weight_decay=1e-3)
         bind = ModuleBinding(x, layers, gate=gate)
         tr.barrier()
@@ -398,7 +398,8 @@ def _graph_worker(rank, world, port, variant, gate, use_graph, q):
 @pytest.mark.parametrize("variant,gate", [("auto", "layer"), ("auto", "model"), ("twoshot", "layer"),
                                           ("twoshot_ce", "layer"), ("twoshot_cep", "model"), ("tree", "layer"),
                                           ("oneshot", "layer"), ("oneshot_ll", "model"), ("oneshot_l128", "layer"),
-                                          ("twoshot_bulk", "layer"), ("twoshot_bulk", "model")])
+                                          ("twoshot_bulk", "layer"), ("twoshot_bulk", "model"),
+                                          ("twoshot_l128", "model")])
 def test_graph_replay_multi_gpu_matches_oracle(variant, gate):
     out = _spawn(_graph_worker, _ngpu(), variant, gate, True)
     for rank, bad, status in out:

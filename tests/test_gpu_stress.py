@@ -113,7 +113,7 @@ def _fold_stress_worker(rank, world, port, variant, iters, q):
             [4099, 1 << 18, (1 << 22) + 12, 3 << 20]
         hyper = dict(lr=0.01, momentum=0.9, weight_decay=5e-4)
         x = DeviceExchange(tr, elems, mode="fast32", variant=variant, chunk_elems=16384,
-                           flags=("allow_l128",) if variant == "oneshot_l128" else (), **hyper)
+                           flags=("allow_l128",) if "l128" in variant else (), **hyper)
         w = [O.seeded_fill(42 ^ l, n, 1.0 / np.sqrt(n)).astype(np.float32) for l, n in enumerate(elems)]
         v = [np.zeros(n, np.float32) for n in elems]
         for l in range(len(elems)):
@@ -154,7 +154,7 @@ def _fold_stress_worker(rank, world, port, variant, iters, q):
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("variant", ["oneshot_ll", "oneshot_l128", "twoshot_bulk", "twoshot"])
+@pytest.mark.parametrize("variant", ["oneshot_ll", "oneshot_l128", "twoshot_bulk", "twoshot", "twoshot_l128"])
 def test_concurrent_fold_stress(variant):
     """Hundreds of back-to-back iterations, no host synchronisation between them (only
     the per-layer gates), fresh gradients each: bit-exact with the oracle at the end."""

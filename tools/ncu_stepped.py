@@ -52,7 +52,7 @@ def main():
         trs = [world.transport(r) for r in range(N)]
         xs = [DeviceExchange(tr, elems, mode=args.mode, variant=variant, chunk_elems=16384, lr=0.01,
                              momentum=0.9, weight_decay=5e-4, max_ctas=args.ctas,
-                             flags=("allow_l128",) if variant == "oneshot_l128" else ()) for tr in trs]
+                             flags=("allow_l128",) if "l128" in variant else ()) for tr in trs]
         for x in xs:
             x.connect()
             x.model.zero_()
@@ -75,6 +75,11 @@ def main():
                         sync()
                     for r in range(N):
                         xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=_lib.PHASE_DOWN)
+                        sync()
+                elif variant == "twoshot_l128":  # push, owner, install
+                    for ph in (_lib.PHASE_PUSH, _lib.PHASE_OWNER, _lib.PHASE_DOWN):
+                        for r in range(N):
+                            xs[r].launch(l, k, g[r], stream=trs[r].stream, phases=ph)
                         sync()
                 else:
                     for r in range(N):

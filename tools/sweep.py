@@ -56,7 +56,8 @@ def main():
     while b <= args.max_mb * 2 ** 20:
         sizes.append(b)
         b *= 4
-    elems = [s // 4 for s in sizes]
+    esz = 8 if args.mode == "ref64" else 4  # ref64: the reference's native f64 elements
+    elems = [s // esz for s in sizes]
     variants = args.variants.split(",")
     out = []
     tr = DistTransport(rank, world, local, timeout_s=30.0)
@@ -64,11 +65,11 @@ def main():
     seg = 16
     for v in variants:
         if v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "nvls", "oneshot", "oneshot_ll", "oneshot_l128",
-                 "twoshot_bulk"):
+                 "twoshot_bulk", "twoshot_l128"):
             xs[v] = DeviceExchange(tr, elems, mode=args.mode, variant=v, chunk_elems=args.chunk, lr=0.01,
                                    momentum=0.9, weight_decay=5e-4, seg_base=seg, max_ctas=args.ctas,
                                    flags=tuple(f for f in args.xflags.split(",") if f)
-                                   + (("allow_l128",) if v == "oneshot_l128" else ()))
+                                   + (("allow_l128",) if "l128" in v else ()))
             seg += 2
     tr.barrier()
     for x in xs.values():
@@ -82,7 +83,7 @@ def main():
         return float(t.item())
 
     for li, n in enumerate(elems):
-        g = torch.randn(n, device=dev) * 1e-3
+        g = torch.randn(n, device=dev, dtype=torch.float64 if esz == 8 else torch.float32) * 1e-3
         for v in variants:
             times = []
             for it in range(args.warmup + args.iters):
@@ -113,11 +114,11 @@ def main():
                 if it >= args.warmup:
                     times.append(e0.elapsed_time(e1))
             ms = tmax(statistics.median(times))
-            nbytes = n * 4
+            nbytes = n * esz
             bus = 2 * (world - 1) / world * nbytes / (ms / 1e3) / 1e9 if world > 1 else None
             rec = {"n_gpus": world, "variant": v, "bytes": nbytes, "ms": ms, "busbw_gbs": bus,
                    "frac_of_770": bus / 770.0 if bus else None, "ctas": args.ctas, "chunk_elems": args.chunk,
-                   "update": ("fused " + args.mode) if v != "nccl" else "none (all-reduce only)",
+                   "update": ("fused " + args.mode) if v != "nccl" else "none (all-reduce only)", "elem_bytes": esz,
                    "hold_us": args.hold_us, "aligned_start": bool(args.align), "xflags": args.xflags or None}
             if rank == 0:
                 print(json.dumps(rec), flush=True)
