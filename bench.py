@@ -63,6 +63,7 @@ def parse():
     p.add_argument("--low-priority-from", type=int, default=0,
                    help="layers with at least this many elements launch on a normal-priority stream (0 = off)")
     p.add_argument("--xflags", default="", help="comma-separated exchange flags (exchange.FLAGS), e.g. bulk_lean")
+    p.add_argument("--l128", default="", help="LO:HI elements sent by the 128-byte-line two-shot (adds allow_l128)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager steps instead of a captured CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -224,6 +225,18 @@ def exchange_by_world(sizes, worlds=(2, 4, 8)) -> dict:
     return out
 
 
+def xflags_of(args) -> tuple:
+    fl = tuple(f for f in args.xflags.split(",") if f)
+    return fl + (("allow_l128",) if args.l128 and "allow_l128" not in fl else ())
+
+
+def l128_of(args) -> tuple:
+    if not args.l128:
+        return (0, 0)
+    lo, hi = args.l128.split(":")
+    return (int(lo), int(hi))
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -269,7 +282,7 @@ def workload_config(world, args):
             "chunk_elems": args.chunk_elems, "large_layers": {"variant": args.large, "ctas": args.large_ctas,
                                                                "chunk_elems": args.large_chunk_elems},
             "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager",
-            "exchange_flags": args.xflags or None}
+            "exchange_flags": args.xflags or None, "l128_range": args.l128 or None}
 
 
 # ------------------------------------------------------------------ model
@@ -407,7 +420,7 @@ def pgx_arm(args):
                           scale=1.0 / world, max_ctas=args.max_ctas,
                           low_priority_from=args.low_priority_from or None, large=args.large,
                           large_ctas=args.large_ctas, large_chunk_elems=args.large_chunk_elems,
-                          flags=tuple(f for f in args.xflags.split(",") if f), **wl["hyper"])
+                          flags=xflags_of(args), l128_range=l128_of(args), **wl["hyper"])
     gate = args.gate if args.gate != "auto" else ("model" if len(sizes) > 16 else "layer")
     bind = ModuleBinding(xchg, model.layers(), gate=gate)
     if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)

@@ -34,7 +34,8 @@ MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE
 
 
 def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20,
-                   oneshot_below: int | None = None, large: str = "ce", ll_below: int = 0) -> str:
+                   oneshot_below: int | None = None, large: str = "ce", ll_below: int = 0,
+                   l128_range: tuple[int, int] = (0, 0)) -> str:
     """Layer-size policy (measured, profiles/r1*_sweep*): the smallest layers are pure
     latency and take the one-shot exchange (one NVLink hop); mid-size layers the SM
     two-shot kernel; layers of `ce_from` elements or more move their shards with the copy
@@ -45,13 +46,17 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
     keeps the SM two-shot for the large layers too (run with a CTA cap and big chunks,
     see DeviceExchange `large_ctas`); large="cep" moves the reduce-scatter by copy engine
     and runs fold + update + all-gather as the SM owner kernel on a capped grid;
-    large="bulk" moves every byte with TMA bulk copies from a capped grid (TWOSHOT_BULK)."""
+    large="bulk" moves every byte with TMA bulk copies from a capped grid (TWOSHOT_BULK).
+    `l128_range` = [lo, hi) elements sent by the fence-free 128-byte-line two-shot
+    (TWOSHOT_L128; DeviceExchange passes it only with the allow_l128 flag)."""
     if oneshot_below is None:  # one-shot moves (N-1)*S per GPU: the crossover shrinks with N
         oneshot_below = (1 << 20) // max(world, 1)  # N=4: 1 MB layers (profiles/r2b_sweep_n4)
     if world > 1 and elems < tree_below:
         return "tree"
     if world > 1 and elems <= ll_below:  # fence-free LL words: lowest latency up to ~256 KB
         return "oneshot_ll"
+    if world > 1 and l128_range[0] <= elems < l128_range[1]:
+        return "twoshot_l128"
     if world > 1 and elems < oneshot_below:
         return "oneshot"
     if world > 1 and elems >= ce_from:
@@ -66,7 +71,7 @@ class DeviceExchange:
                  tree_below: int = 0, low_priority_from: int | None = None, large: str = "ce",
                  large_from: int = 1 << 20, large_ctas: int = 0, large_chunk_elems: int = 0,
                  layer_chunk_elems=None, layer_max_ctas=None, ce_parts: int = 0, ce_rs_streams: int = 0,
-                 flags=()):
+                 flags=(), l128_range: tuple[int, int] = (0, 0)):
         """variant: one name, a per-layer list, or "auto" (choose_variant; `large` = "ce" or
         "sm" for layers of >= `large_from` elements).  Layers of >= `large_from` elements get
         `large_chunk_elems` / `large_ctas` (0 = the global chunk_elems / max_ctas): fewer CTAs
@@ -85,8 +90,9 @@ class DeviceExchange:
         L = len(self.layer_elems)
         if isinstance(variant, str) and variant == "auto":
             ll = (1 << 16) if mode != "ref64" else 0
-            variants = [choose_variant(n, self.world, tree_below, ce_from=large_from, large=large, ll_below=ll)
-                        for n in self.layer_elems]
+            l128 = tuple(l128_range) if ("allow_l128" in flags and mode != "ref64") else (0, 0)
+            variants = [choose_variant(n, self.world, tree_below, ce_from=large_from, large=large, ll_below=ll,
+                                       l128_range=l128) for n in self.layer_elems]
         elif isinstance(variant, str):
             variants = [variant] * L
         else:
