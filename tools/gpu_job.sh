@@ -1,56 +1,28 @@
 #!/bin/bash
-# The current GPU job (overwritten per gpurun call; the outputs land in gpurun_out/ and the
-# ones worth keeping are copied to profiles/).  r5t (2 GPUs): ncu of the exchange kernels
-# stepped on one GPU (N=4 emulated, --set full) and across two GPUs (N=2, NVLink byte
-# counters), compute-sanitizer on the stepped exchanges, the 2-GPU multi/stress suite.
+# The current GPU job (overwritten per gpurun call; outputs land in gpurun_out/, the ones worth
+# keeping are copied to profiles/).  r5u (4 GPUs): TWOSHOT_L128 at 64-256 MB; in-step AlexNet /
+# GoogLeNet with the 128-byte-line two-shot for mid-size (and all) layers; configs[0]/[1] lines.
 cd "$(dirname "$0")/.." || exit 1
 O=gpurun_out
 mkdir -p $O
-FC6=37752832
-
-# 1. ncu --set full, N=4 emulated on GPU 0 (each command first exits 0 without ncu)
-run() {  # name variants regex skip count [elems]
-  local name=$1 var=$2 rx=$3 sk=$4 cnt=$5 el=${6:-$FC6}
-  local cmd="python tools/ncu_stepped.py --world 4 --elems $el --variants $var --iters 2"
-  CUDA_VISIBLE_DEVICES=0 timeout 300 $cmd > $O/r5t_plain_$name.log 2>&1 && \
-  CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-      -k regex:"$rx" -s $sk -c $cnt -o $O/r5t_ncu_$name $cmd > $O/r5t_ncu_$name.log 2>&1
-  echo "ncu $name rc=$?"
-  # the .ncu-rep files are tens of MB: keep the text pages, drop the report (64 MiB pull cap)
-  ncu -i $O/r5t_ncu_$name.ncu-rep --page details --csv > $O/r5t_ncu_${name}_details.csv 2>/dev/null
-  ncu -i $O/r5t_ncu_$name.ncu-rep --page raw --csv > $O/r5t_ncu_${name}_raw.csv 2>/dev/null
-  rm -f $O/r5t_ncu_$name.ncu-rep
-}
-run twoshot4 twoshot "k_twoshot<.int.4," 8 5
-run bulk4 twoshot_bulk "k_twoshot_bulk<.int.4," 8 5
-run ce4 twoshot_ce "k_owner_local<.int.4," 16 4
-run ll4 oneshot_ll "k_oneshot_ll<.int.4>" 8 5 65536
-run oneshot4 oneshot "k_oneshot<.int.4," 8 5 262144
-run tree4 tree "k_tree_(up|down)<" 8 6
-
-# 2. NVLink bytes: N=2 stepped across GPUs 0 and 1 (push / owner phases never wait on a
-#    peer when launched in this order); ncu profiles device 0's launches only
-M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes_data_user.sum
-for v in twoshot twoshot_bulk oneshot tree; do
-  el=$FC6; [ $v = oneshot ] && el=262144
-  cmd="python tools/ncu_stepped.py --world 2 --devices 0,1 --elems $el --variants $v --iters 2 --check"
-  timeout 300 $cmd > $O/r5t_plain_nvl_$v.log 2>&1 && \
-  timeout 900 ncu --metrics $M --clock-control none --devices 0 --kernel-name-base demangled -k regex:"k_(twoshot|oneshot|tree)" \
-      --csv $cmd > $O/r5t_ncu_nvl_$v.csv 2> $O/r5t_ncu_nvl_$v.err
-  echo "nvl $v rc=$?"
+for n in 2 4; do
+  CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 600 torchrun --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2980$n \
+    tools/sweep.py --min-kb 65536 --max-mb 256 --variants twoshot_l128,twoshot,twoshot_ce,nccl > $O/r5u_sweep_large_n$n.jsonl 2> $O/r5u_sweep_large_n$n.err
+  echo "sweep n=$n rc=$?"
 done
-
-# 3. compute-sanitizer on the stepped exchanges (small layers, every variant, checked vs oracle)
-SM="520,25050,400500,5010"
-for tool in memcheck racecheck synccheck; do
-  CUDA_VISIBLE_DEVICES=0 timeout 900 compute-sanitizer --tool $tool --kernel-name kns=pgx --print-limit 50 \
-      python tools/ncu_stepped.py --world 4 --elems $SM --variants twoshot,oneshot,oneshot_ll,twoshot_bulk,twoshot_ce,tree \
-      --iters 2 --check > $O/r5t_sanitizer_$tool.full 2>&1
-  echo "sanitizer $tool rc=$?"
-  head -c 200000 $O/r5t_sanitizer_$tool.full > $O/r5t_sanitizer_$tool.log; rm -f $O/r5t_sanitizer_$tool.full
-done
-
-# 4. the 2-GPU multi / stress suite with test ids in the log
-timeout 1500 python -m pytest tests/test_gpu_multi.py tests/test_gpu_stress.py -m gpu -rA -q > $O/r5t_pytest_multi_4gpus.log 2>&1
-echo "pytest rc=$?"
+TR="torchrun --nproc-per-node 4 --master-addr 127.0.0.1"
+B="bench.py --gpus 4 --steps 30 --warmup 5 --no-cpu-baseline"
+timeout 900 $TR --master-port 29821 $B --l128 65537:1048576 > $O/r5u_bench4_l128mid.json 2> $O/r5u_bench4_l128mid.err; echo "b1 rc=$?"
+timeout 900 $TR --master-port 29822 $B --l128 65537:4000000000 > $O/r5u_bench4_l128all.json 2> $O/r5u_bench4_l128all.err; echo "b2 rc=$?"
+timeout 900 $TR --master-port 29823 $B > $O/r5u_bench4_ce.json 2> $O/r5u_bench4_ce.err; echo "b3 rc=$?"
+timeout 900 $TR --master-port 29824 $B --workload googlenet > $O/r5u_gbench4.json 2> $O/r5u_gbench4.err; echo "g1 rc=$?"
+timeout 900 $TR --master-port 29825 $B --workload googlenet --l128 65537:1048576 > $O/r5u_gbench4_l128mid.json 2> $O/r5u_gbench4_l128mid.err; echo "g2 rc=$?"
+T2="torchrun --nproc-per-node 2 --master-addr 127.0.0.1"
+CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29826 bench.py --gpus 2 --steps 30 --warmup 5 --no-cpu-baseline --l128 65537:1048576 > $O/r5u_bench2_l128mid.json 2> $O/r5u_bench2_l128mid.err; echo "b4 rc=$?"
+CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29827 bench.py --gpus 2 --steps 30 --warmup 5 --no-cpu-baseline > $O/r5u_bench2_ce.json 2> $O/r5u_bench2_ce.err; echo "b5 rc=$?"
+# configs[0] LeNet-5 at 2 ranks, configs[1] cifar10_quick at 4 ranks: product arm + reference arm
+CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29828 bench.py --gpus 2 --workload lenet --steps 50 --warmup 10 > $O/r5u_lenet2.json 2> $O/r5u_lenet2.err; echo "l1 rc=$?"
+CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29829 bench.py --gpus 2 --workload lenet --impl reference --steps 20 --warmup 3 > $O/r5u_lenet2_ref.json 2> $O/r5u_lenet2_ref.err; echo "l2 rc=$?"
+timeout 900 $TR --master-port 29830 bench.py --gpus 4 --workload cifar10_quick --steps 50 --warmup 10 > $O/r5u_cifar4.json 2> $O/r5u_cifar4.err; echo "c1 rc=$?"
+timeout 900 $TR --master-port 29831 bench.py --gpus 4 --workload cifar10_quick --impl reference --steps 20 --warmup 3 > $O/r5u_cifar4_ref.json 2> $O/r5u_cifar4_ref.err; echo "c2 rc=$?"
 echo done
