@@ -729,19 +729,21 @@ def pgx_arm(args):
              "twoshot_cep": "k_twoshot owner items + copy-engine reduce-scatter",
              "twoshot_bulk": "k_twoshot_bulk (TMA bulk copies, capped grid)",
              "tree": "k_tree_up/k_tree_down", "nvls": "k_nvls (multimem)",
-             "oneshot": "k_oneshot"}[xchg.variants[L_DOM]]
+             "oneshot": "k_oneshot", "twoshot_l128": "k_twoshot_l128 (128-byte lines, fence-free)",
+             "oneshot_ll": "k_oneshot_ll", "oneshot_l128": "k_oneshot_l128"}[xchg.variants[L_DOM]]
     what = "%s, layer %d (%d params): fold + fused momentum update%s" % (
         kname, L_DOM, sizes[L_DOM], " + reduce-scatter/all-gather over NVLink" if world > 1 else "")
     measured_in = (("median of CUDA events captured in the step graph, %d replays after the timed region" % len(durs))
                    if graph is not None else "CUDA events in every timed eager step")
-    traffic = ncu_traffic(kname.split()[0], world, sizes[L_DOM])
+    traffic, traffic_nvl, traffic_src = ncu_traffic(kname.split()[0], world, sizes[L_DOM])
     roof = None
     if avg and world == 1:  # one GPU: the fused update is an HBM stream
         peak, peak_src = hbm_peak()
         ach = hbm / (avg / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": what, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                 "traffic": traffic, "algorithmic_bytes_per_launch": hbm, "avg_launch_ms_in_step": avg, "in_step_ms_samples": [round(d, 4) for d in durs],
-                "peak_source": peak_src, "launch_share_of_step": avg / (ms / args.steps), "measured_in": measured_in}
+                "peak_source": peak_src, "launch_share_of_step": avg / (ms / args.steps), "measured_in": measured_in,
+                "traffic_source": traffic_src}
         if iso:
             roof["isolated_launch_ms"] = statistics.median(iso)
             roof["isolated_achieved"] = hbm / (statistics.median(iso) / 1e3) / 1e9
@@ -757,7 +759,7 @@ def pgx_arm(args):
                 "measured_in": measured_in + "; in-step time includes waiting for the slowest rank's gradient",
                 "isolated_ms": iso_ms, "isolated_achieved": nvl / (iso_ms / 1e3) / 1e9,
                 "isolated_frac": nvl / (iso_ms / 1e3) / 1e9 / NVLINK_PEAK_GBS,
-                "hbm_bytes_per_launch": hbm}
+                "hbm_bytes_per_launch": hbm, "traffic_nvlink_tx": traffic_nvl, "traffic_source": traffic_src}
     line = {"metric": wl["metric"], "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
@@ -1010,15 +1012,21 @@ def comparison_arm(args):
 
 
 def ncu_traffic(kernel: str, world: int, layer_params: int):
-    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture
-    (profiles/ncu_traffic.json), when one exists for this kernel/world/layer; else None."""
+    """(dram read+write bytes, NVLink tx bytes, source) per launch of the dominant kernel from
+    the committed ncu captures (profiles/ncu_traffic.json) for this kernel/world/layer; None
+    entries where no capture exists.  N=2 entries come from a run across two GPUs (NVLink
+    counters included); 4 ranks stepped on one GPU are only a fallback (local peer stores)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             table = json.load(fh)
     except Exception:  # noqa: BLE001
-        return None
-    rec = table.get(f"{kernel}/N{world}/{layer_params}")
-    return None if rec is None else rec["dram_read_bytes"] + rec["dram_write_bytes"]
+        return None, None, None
+    for key in (f"{kernel}/N{world}/{layer_params}", f"{kernel}/N{world}stepped/{layer_params}"):
+        rec = table.get(key)
+        if rec is not None:
+            return rec["dram_read_bytes"] + rec["dram_write_bytes"], rec.get("nvltx_bytes"), \
+                "profiles/ncu_traffic.json " + key
+    return None, None, None
 
 
 def hbm_peak():
