@@ -40,6 +40,7 @@ def wl_of(args):
 def global_batch(wl, world):
     return wl["global_batch"] if "global_batch" in wl else wl["per_gpu_batch"] * world
 NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+L128_BAND = ((1 << 16) + 1, 1 << 20)  # = exchange.L128_BAND (kept import-free for the reference arm)
 
 
 def parse():
@@ -63,7 +64,8 @@ def parse():
     p.add_argument("--low-priority-from", type=int, default=0,
                    help="layers with at least this many elements launch on a normal-priority stream (0 = off)")
     p.add_argument("--xflags", default="", help="comma-separated exchange flags (exchange.FLAGS), e.g. bulk_lean")
-    p.add_argument("--l128", default="", help="LO:HI elements sent by the 128-byte-line two-shot (adds allow_l128)")
+    p.add_argument("--l128", default="%d:%d" % L128_BAND,
+                   help="LO:HI elements sent by the 128-byte-line two-shot (adds allow_l128); '' = off")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager steps instead of a captured CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")

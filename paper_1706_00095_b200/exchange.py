@@ -33,6 +33,12 @@ FLAGS = {"ce_rs_parts": _lib.XF_CE_RS_PARTS, "tma": _lib.XF_TMA, "oneshot_small_
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 
+# Layers of (64 K, 1 M) elements take the 128-byte-line two-shot when the caller opts in
+# (allow_l128): 1-16 MB device time below NCCL's all-reduce at N=2 and N=4
+# (profiles/r5s_sweep_mid_n*.jsonl); slower than the SM two-shot at 64 MB+ (r5u_sweep_large).
+L128_BAND = ((1 << 16) + 1, 1 << 20)
+
+
 def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1 << 20,
                    oneshot_below: int | None = None, large: str = "ce", ll_below: int = 0,
                    l128_range: tuple[int, int] = (0, 0)) -> str:

@@ -1,10 +1,10 @@
 """The exchange configuration bench.py runs, compared bit for bit with the oracle.
 
-bench.py builds `DeviceExchange(variant="auto", chunk_elems=16384, scale=1/N, large="ce")`
-over the AlexNet layer list (and GoogLeNet's 64 layers with the whole-model gate).  At
-N >= 2 that sends fc6/fc7/fc8 to the copy-engine two-shot with its owner shard split into
-pipelined parts (`ce_split`), conv2-5 to the SM two-shot / one-shot with size-scaled
-chunks, and conv1 to the LL one-shot.  These tests drive exactly that plan, ranks
+bench.py builds `DeviceExchange(variant="auto", chunk_elems=16384, scale=1/N, large="ce",
+flags=("allow_l128",), l128_range=L128_BAND)` over the AlexNet layer list (and GoogLeNet's
+64 layers with the whole-model gate).  At N >= 2 that sends fc6/fc7/fc8 to the copy-engine
+two-shot with its owner shard split into pipelined parts (`ce_split`), conv2-5 to the
+128-byte-line two-shot (TWOSHOT_L128), and conv1 to the LL one-shot.  These tests drive exactly that plan, ranks
 emulated on ONE GPU with every phase launched in dependency order (test_gpu_exchange's
 single-GPU hazard rule), and require the weights every rank holds to equal the
 oracle's tree-order fold + update (pipelined.py:158-203, sgd.py:27-33; the bar is the
@@ -46,15 +46,20 @@ def _bits_equal(t, a):
 
 
 def _expected_variants(sizes, N, mode):
-    from paper_1706_00095_b200.exchange import choose_variant
+    from paper_1706_00095_b200.exchange import L128_BAND, choose_variant
 
     ll = (1 << 16) if mode != "ref64" else 0
-    return [choose_variant(n, N, 0, ce_from=1 << 20, large="ce", ll_below=ll) for n in sizes]
+    band = L128_BAND if mode != "ref64" else (0, 0)
+    return [choose_variant(n, N, 0, ce_from=1 << 20, large="ce", ll_below=ll, l128_range=band) for n in sizes]
 
 
 def _run(N, sizes, mode, iters, gate):
+    from paper_1706_00095_b200.exchange import L128_BAND
+
     hyper = HYPER if mode == "fast32" else dict(lr=0.05)
-    world, trs, xs = build(N, sizes, mode, "auto", chunk_elems=16384, **hyper)
+    # bench.py's defaults: --l128 = L128_BAND (with the allow_l128 opt-in), large layers "ce"
+    world, trs, xs = build(N, sizes, mode, "auto", chunk_elems=16384, flags=("allow_l128",), l128_range=L128_BAND,
+                           **hyper)
     assert xs[0].variants == _expected_variants(sizes, N, mode)
     w = [O.seeded_fill(42 ^ l, n, 1.0 / np.sqrt(n)).astype(np.float32) for l, n in enumerate(sizes)]
     v = [np.zeros(n, np.float32) for n in sizes]

@@ -1,28 +1,36 @@
 #!/bin/bash
 # The current GPU job (overwritten per gpurun call; outputs land in gpurun_out/, the ones worth
-# keeping are copied to profiles/).  r5u (4 GPUs): TWOSHOT_L128 at 64-256 MB; in-step AlexNet /
-# GoogLeNet with the 128-byte-line two-shot for mid-size (and all) layers; configs[0]/[1] lines.
+# keeping are copied to profiles/).  r5v (4 GPUs): the driver's 1-GPU suite + smoke on the
+# new default (L128 band), bench lines N=1/2/4 + GoogLeNet, the N=1 launch list, ncu of the
+# 128-byte-line two-shot (stepped N=4 on one GPU; N=2 across GPUs with NVLink counters).
 cd "$(dirname "$0")/.." || exit 1
 O=gpurun_out
 mkdir -p $O
-for n in 2 4; do
-  CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 600 torchrun --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2980$n \
-    tools/sweep.py --min-kb 65536 --max-mb 256 --variants twoshot_l128,twoshot,twoshot_ce,nccl > $O/r5u_sweep_large_n$n.jsonl 2> $O/r5u_sweep_large_n$n.err
-  echo "sweep n=$n rc=$?"
-done
-TR="torchrun --nproc-per-node 4 --master-addr 127.0.0.1"
-B="bench.py --gpus 4 --steps 30 --warmup 5 --no-cpu-baseline"
-timeout 900 $TR --master-port 29821 $B --l128 65537:1048576 > $O/r5u_bench4_l128mid.json 2> $O/r5u_bench4_l128mid.err; echo "b1 rc=$?"
-timeout 900 $TR --master-port 29822 $B --l128 65537:4000000000 > $O/r5u_bench4_l128all.json 2> $O/r5u_bench4_l128all.err; echo "b2 rc=$?"
-timeout 900 $TR --master-port 29823 $B > $O/r5u_bench4_ce.json 2> $O/r5u_bench4_ce.err; echo "b3 rc=$?"
-timeout 900 $TR --master-port 29824 $B --workload googlenet > $O/r5u_gbench4.json 2> $O/r5u_gbench4.err; echo "g1 rc=$?"
-timeout 900 $TR --master-port 29825 $B --workload googlenet --l128 65537:1048576 > $O/r5u_gbench4_l128mid.json 2> $O/r5u_gbench4_l128mid.err; echo "g2 rc=$?"
+CUDA_VISIBLE_DEVICES=0 timeout 1200 python -m pytest tests -m gpu -x -q > $O/r5v_pytest_gpu_1gpu.log 2>&1; echo "suite rc=$?"
+CUDA_VISIBLE_DEVICES=0 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/r5v_smoke.log 2>&1; echo "smoke rc=$?"
+CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py > $O/r5v_bench1.json 2> $O/r5v_bench1.err; echo "b1 rc=$?"
+CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py --impl reference > $O/r5v_bench1_ref.json 2> $O/r5v_bench1_ref.err; echo "b1ref rc=$?"
 T2="torchrun --nproc-per-node 2 --master-addr 127.0.0.1"
-CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29826 bench.py --gpus 2 --steps 30 --warmup 5 --no-cpu-baseline --l128 65537:1048576 > $O/r5u_bench2_l128mid.json 2> $O/r5u_bench2_l128mid.err; echo "b4 rc=$?"
-CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29827 bench.py --gpus 2 --steps 30 --warmup 5 --no-cpu-baseline > $O/r5u_bench2_ce.json 2> $O/r5u_bench2_ce.err; echo "b5 rc=$?"
-# configs[0] LeNet-5 at 2 ranks, configs[1] cifar10_quick at 4 ranks: product arm + reference arm
-CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29828 bench.py --gpus 2 --workload lenet --steps 50 --warmup 10 > $O/r5u_lenet2.json 2> $O/r5u_lenet2.err; echo "l1 rc=$?"
-CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29829 bench.py --gpus 2 --workload lenet --impl reference --steps 20 --warmup 3 > $O/r5u_lenet2_ref.json 2> $O/r5u_lenet2_ref.err; echo "l2 rc=$?"
-timeout 900 $TR --master-port 29830 bench.py --gpus 4 --workload cifar10_quick --steps 50 --warmup 10 > $O/r5u_cifar4.json 2> $O/r5u_cifar4.err; echo "c1 rc=$?"
-timeout 900 $TR --master-port 29831 bench.py --gpus 4 --workload cifar10_quick --impl reference --steps 20 --warmup 3 > $O/r5u_cifar4_ref.json 2> $O/r5u_cifar4_ref.err; echo "c2 rc=$?"
+T4="torchrun --nproc-per-node 4 --master-addr 127.0.0.1"
+CUDA_VISIBLE_DEVICES=0,1 timeout 900 $T2 --master-port 29841 bench.py --gpus 2 --no-cpu-baseline > $O/r5v_bench2.json 2> $O/r5v_bench2.err; echo "b2 rc=$?"
+timeout 900 $T4 --master-port 29842 bench.py --gpus 4 --no-cpu-baseline > $O/r5v_bench4.json 2> $O/r5v_bench4.err; echo "b4 rc=$?"
+timeout 900 $T4 --master-port 29843 bench.py --gpus 4 --no-cpu-baseline --workload googlenet > $O/r5v_gbench4.json 2> $O/r5v_gbench4.err; echo "g4 rc=$?"
+CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+  --log-file $O/r5v_launches_n1.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/r5v_ncu_launches.log 2>&1; echo "launches rc=$?"
+# ncu of TWOSHOT_L128: fc8-size (16 MB) and conv3-size layers, stepped
+for el in 4097000 885120; do
+  cmd="python tools/ncu_stepped.py --world 4 --elems $el --variants twoshot_l128 --iters 2 --check"
+  CUDA_VISIBLE_DEVICES=0 timeout 300 $cmd > $O/r5v_plain_l128_$el.log 2>&1 && \
+  CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k regex:"k_twoshot_l128" -s 12 -c 6 -o $O/r5v_ncu_l128_$el $cmd > $O/r5v_ncu_l128_$el.log 2>&1
+  echo "ncu l128 $el rc=$?"
+  ncu -i $O/r5v_ncu_l128_$el.ncu-rep --page raw --csv > $O/r5v_ncu_l128_${el}_raw.csv 2>/dev/null
+  ncu -i $O/r5v_ncu_l128_$el.ncu-rep --page details --csv > $O/r5v_ncu_l128_${el}_details.csv 2>/dev/null
+  rm -f $O/r5v_ncu_l128_$el.ncu-rep
+done
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,nvltx__bytes.sum,nvlrx__bytes.sum,nvltx__bytes_data_user.sum,nvlrx__bytes_data_user.sum
+cmd="python tools/ncu_stepped.py --world 2 --devices 0,1 --elems 4097000 --variants twoshot_l128 --iters 2 --check"
+timeout 300 $cmd > $O/r5v_plain_nvl_l128.log 2>&1 && \
+timeout 900 ncu --metrics $M --clock-control none --devices 0 --kernel-name-base demangled -k regex:"k_twoshot_l128" \
+    --csv $cmd > $O/r5v_ncu_nvl_l128.csv 2> $O/r5v_ncu_nvl_l128.err; echo "nvl l128 rc=$?"
 echo done
