@@ -90,6 +90,8 @@ struct XArgs {
   uint32_t push_items, items;
   uint32_t item_begin, item_end;       // claimed range (phase selection)
   uint64_t olo, ohi;                   // TWOSHOT_CE owner sub-range (ohi == 0: the whole shard)
+  uint64_t CHo;                        // TWOSHOT_L128: lines per owner item
+  uint32_t Co;                         // TWOSHOT_L128: owner items
   int single_buffer;                   // rx parity fixed at 0 (TWOSHOT_CEP: host-addressed copies)
   int bulk_lean;                       // TWOSHOT_BULK: the lean footprint (PGX_XF_BULK_LEAN)
   unsigned long long* trace;           // debug: per-item globaltimer stamps (pgx_xchg_set_trace) or null
@@ -1190,7 +1192,7 @@ __global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_twoshot_l128(XArgs
   };
   const int nv = k < 7 ? 4 : 2;  // values carried by this lane
   constexpr int NP = N > 1 ? N - 1 : 1;
-  const uint32_t Cs = a.C, owner_end = a.push_items + Cs;
+  const uint32_t owner_end = a.push_items + a.Co;
   float* const wbase = static_cast<float*>(a.model[me]);
   const bool fast = a.mode == PGX_MODE_FAST32;
   while (true) {
@@ -1202,7 +1204,7 @@ __global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_twoshot_l128(XArgs
       kind = 0;
       c = it / NP;
       j = (me + 1 + (int)(it % NP)) % N;
-    } else if (it < owner_end) {
+    } else if (it < owner_end) {  // owner items: CHo lines each (the heavier work, finer grain)
       kind = 1;
       c = it - a.push_items;
       j = me;
@@ -1213,7 +1215,8 @@ __global__ void __launch_bounds__(kThreads, N <= 4 ? 2 : 1) k_twoshot_l128(XArgs
       j = (me + 1 + (int)(i2 % NP)) % N;
     }
     const uint64_t s_lo = (uint64_t)j * Ls, s_hi = min(s_lo + Ls, lines);
-    const uint64_t l_lo = s_lo + (uint64_t)c * a.CH, l_hi = min(l_lo + a.CH, s_hi);
+    const uint64_t ch = kind == 1 ? a.CHo : a.CH;
+    const uint64_t l_lo = s_lo + (uint64_t)c * ch, l_hi = min(l_lo + ch, s_hi);
     bool failed = false;
     for (uint64_t l0 = l_lo + (uint64_t)warp * 4; l0 < l_hi && !failed; l0 += (uint64_t)nwarps * 4) {
       const uint64_t line = l0 + q;
@@ -1639,6 +1642,8 @@ struct LayerPlan {
   uint32_t dflag = 0;    // tree down flags index (in mflags)
   uint32_t push_items = 0, items = 0, down_items = 0;
   uint32_t expected = 0; // remote chunk arrivals per epoch
+  uint64_t CHo = 0;      // TWOSHOT_L128: lines per owner item (finer than the push items)
+  uint32_t Co = 0;       // TWOSHOT_L128: owner items
   int grid = 0, down_grid = 0;
   uint64_t nvlink_bytes = 0, hbm_bytes = 0;
 };
@@ -1760,6 +1765,8 @@ XArgs base_args(pgx_xchg* x, int l, uint32_t iteration) {
   a.parity = iteration & 1;
   a.push_items = P.push_items;
   a.items = P.items;
+  a.CHo = P.CHo;
+  a.Co = P.Co;
   a.lr = x->cfg.lr;
   a.scale = x->cfg.scale;
   a.mu = x->cfg.momentum;
@@ -2544,13 +2551,18 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       if (ch_given) CH = std::max<uint64_t>(1, cfg->layer_chunk_elems[l] / kL128Vals);
       P.CH = CH;
       P.C = (uint32_t)((Ls + CH - 1) / CH);  // chunks per shard (ragged last shard: empty items)
+      // owner items fold N-1 polled lines and store N-1 copies per line: (N-1)x finer than
+      // the push items so the owner phase spreads over as many CTAs as the push phase
+      P.CHo = std::max<uint64_t>(64, align_up((CH + std::max(N - 1, 1) - 1) / std::max(N - 1, 1), 4));
+      if (P.CHo > CH) P.CHo = CH;
+      P.Co = (uint32_t)((Ls + P.CHo - 1) / P.CHo);
       P.K = N;
       P.rx_off = rxoff;
       rxoff = align_up(rxoff + 2 * ((uint64_t)N * P.sl + agl), kAlignElems);
       P.rxflag_off = rxfoff;  // no flags: the epoch rides in every line
       P.push_items = (uint32_t)(N - 1) * P.C;
       P.down_items = (uint32_t)(N - 1) * P.C;  // install items (PGX_PHASE_DOWN)
-      P.items = P.push_items + P.C + P.down_items;
+      P.items = P.push_items + P.Co + P.down_items;
       P.expected = 0;  // this rank's own install items complete the layer
       P.grid = (int)std::min<uint64_t>(P.items, cap);
       const uint64_t my_lines = std::min(lines, (uint64_t)(x->rank + 1) * Ls) - std::min(lines, (uint64_t)x->rank * Ls);
@@ -2804,7 +2816,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
   if (P.variant == PGX_VARIANT_TWOSHOT_L128) {
     // items: [0, push) reduce-scatter, [push, push + C) owner, [push + C, items) install
     xrecord(x->ready[l], s);
-    const uint32_t own_end = P.push_items + P.C;
+    const uint32_t own_end = P.push_items + P.Co;
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : (phases & PGX_PHASE_OWNER) ? P.push_items : own_end;
     a.item_end = (phases & PGX_PHASE_DOWN) ? P.items : (phases & PGX_PHASE_OWNER) ? own_end : P.push_items;
     if (a.item_end > a.item_begin) {
