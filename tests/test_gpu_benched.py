@@ -53,10 +53,10 @@ def _expected_variants(sizes, N, mode):
     return [choose_variant(n, N, 0, ce_from=1 << 20, large="ce", ll_below=ll, l128_range=band) for n in sizes]
 
 
-def _run(N, sizes, mode, iters, gate):
+def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER):
     from paper_1706_00095_b200.exchange import L128_BAND
 
-    hyper = HYPER if mode == "fast32" else dict(lr=0.05)
+    hyper = fast_hyper if mode == "fast32" else dict(lr=0.05)
     # bench.py's defaults: --l128 = L128_BAND (with the allow_l128 opt-in), large layers "ce"
     world, trs, xs = build(N, sizes, mode, "auto", chunk_elems=16384, flags=("allow_l128",), l128_range=L128_BAND,
                            **hyper)
@@ -76,8 +76,8 @@ def _run(N, sizes, mode, iters, gate):
             pieces = [[torch.from_numpy(g[:cut]).cuda(), torch.from_numpy(g[cut:]).cuda()] for g in grads]
             stepped_layer(xs, trs, l, k, pieces, gate=(gate == "layer"))
             if mode == "fast32":
-                w[l], v[l] = O.exchange_iteration(grads, w[l], 0.01, mode, state=v[l], scale=1.0 / N,
-                                                  momentum=0.9, weight_decay=5e-4)
+                w[l], v[l] = O.exchange_iteration(grads, w[l], hyper["lr"], mode, state=v[l], scale=1.0 / N,
+                                                  momentum=hyper["momentum"], weight_decay=hyper["weight_decay"])
             else:
                 w[l] = O.exchange_iteration(grads, w[l], 0.05, mode).astype(np.float32)
             del pieces, grads
@@ -125,3 +125,14 @@ def test_googlenet_auto_plan_model_gate_matches_oracle(cuda, N):
     """GoogLeNet's 64 layers (12 KB .. 8 MB) with the whole-model gate bench.py uses for
     nets of > 16 layers: LL / one-shot / two-shot / copy-engine layers in one step."""
     _run(N, _googlenet_sizes(), "fast32", iters=2, gate="model")
+
+
+@pytest.mark.parametrize("workload,N", [("lenet", 2), ("cifar10_quick", 4)])
+def test_small_net_auto_plans_match_oracle(cuda, workload, N):
+    """BASELINE configs[0] (LeNet-5, 2 ranks) and configs[1] (cifar10_quick, 4 ranks) with
+    their own SGD hyper-parameters (workloads.WORKLOADS), the plan bench.py runs for them."""
+    from workloads import WORKLOADS
+
+    wl = WORKLOADS[workload]
+    sizes = [sum(p.numel() for p in ps) for _, ps in wl["cls"]().layers()]
+    _run(N, sizes, "fast32", iters=3, gate="layer", fast_hyper=wl["hyper"])
