@@ -225,8 +225,11 @@ enum pgx_xchg_flag {
   PGX_XF_AUTO_CHUNK_TREE = 8,      /* TREE: size-scaled chunks (measured slower, r3r)        */
   PGX_XF_NO_AUTO_CHUNK_NVLS = 16,  /* NVLS: keep chunk_elems instead of size-scaled chunks   */
   PGX_XF_ALLOW_L128 = 32,          /* permit ONESHOT_L128 / TWOSHOT_L128 layers (sm_100 only) */
-  PGX_XF_BULK_LEAN = 64            /* TWOSHOT_BULK: 256 threads + 64 KB ring per CTA (shares
+  PGX_XF_BULK_LEAN = 64,           /* TWOSHOT_BULK: 256 threads + 64 KB ring per CTA (shares
                                       SMs with the backward) instead of 512 + 224 KB        */
+  PGX_XF_BULK_CE_RS = 128          /* TWOSHOT_BULK: reduce-scatter by the copy engines in
+                                      part-major copies (per-part chunk signals); the kernel
+                                      runs the owner slabs only (fold + update + TMA gather) */
 };
 
 typedef struct pgx_xchg_config {

@@ -33,6 +33,7 @@ VARIANT_TWOSHOT_BULK = 8
 VARIANT_TWOSHOT_L128 = 9
 XF_CE_RS_PARTS, XF_TMA, XF_ONESHOT_SMALL_CHUNKS, XF_AUTO_CHUNK_TREE, XF_NO_AUTO_CHUNK_NVLS, XF_ALLOW_L128 = 1, 2, 4, 8, 16, 32
 XF_BULK_LEAN = 64
+XF_BULK_CE_RS = 128
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p

@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XAr
   constexpr int W = VecT<T>::W;
   constexpr int S = G::kStages;
   const uint32_t epoch = a.iter ? *a.iter + 1 : a.epoch;
-  const int parity = a.iter ? (int)(*a.iter & 1) : a.parity;
+  const int parity = a.single_buffer ? 0 : (a.iter ? (int)(*a.iter & 1) : a.parity);
   extern __shared__ __align__(128) uint8_t ring[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + G::kRing);  // push ring mbarriers
   __shared__ uint32_t s_item;
@@ -1705,6 +1705,7 @@ struct pgx_xchg {
   int ce_parts = 4, ce_rs_streams = 1;             // owner pipelining depth, push streams (measured, r1l)
   bool ce_rs_parts = false;                        // push signals per owner part (signals on ce_rs2)
   bool tma = false;  // TWOSHOT: push / all-gather as TMA bulk copies (PGX_TMA=1; slower fused at N=4, profiles/r1r)
+  bool bulk_ce_rs = false;  // TWOSHOT_BULK: reduce-scatter by the copy engines (PGX_XF_BULK_CE_RS)
   bool oneshot_small_chunks = false;  // PGX_ONESHOT_SMALL_CHUNKS=1: measured slower (profiles/r3v)
   bool auto_chunk_tree = false, auto_chunk_nvls = true;  // size-scaled chunks: NVLS yes, tree no (its pipeline
                                                         // fill grows with the chunk; profiles/r3r)
@@ -2378,6 +2379,85 @@ static int launch_twoshot_cep(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, 
   return PGX_OK;
 }
 
+// TWOSHOT_BULK with PGX_XF_BULK_CE_RS: the reduce-scatter moves by the copy engines (zero
+// SM time) in part-major copies — part p of every peer's shard, then one k_signal_range on a
+// second stream raising exactly the chunk flags that part covers — so the owner kernel
+// (k_twoshot_bulk owner slabs: tree-order fold + fused update + TMA bulk all-gather, capped
+// grid) folds part p while part p+1 is still on the wire.  Receive slots are single-buffered
+// like the other host-addressed variants (a sender rewrites a slot only after gating on this
+// owner's previous all-gather, which follows the owner's reads of the slot).
+constexpr uint32_t kCebParts = 4;
+
+static int launch_bulk_ce_rs(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, int phases) {
+  const int N = x->world, me = x->rank, esz = x->esz;
+  a.single_buffer = 1;
+  a.parity = 0;
+  cudaError_t e = cudaSuccess;
+  const uint32_t cp = (P.C + kCebParts - 1) / kCebParts;  // chunks per part
+  auto shard = [&](int j, uint64_t& lo, uint64_t& hi) {
+    lo = std::min(P.S, (uint64_t)j * P.sl);
+    hi = std::min(P.S, (uint64_t)(j + 1) * P.sl);
+  };
+  if (phases & PGX_PHASE_PUSH) {
+    xwait(x->ce_rs, x->ready[l]);
+    xwait(x->ce_rs2, x->ready[l]);
+    for (uint32_t p = 0; (uint64_t)p * cp < P.C; ++p) {
+      FlagRanges fr{};
+      for (int d = 1; d < N; ++d) {
+        const int j = (me + d) % N;
+        uint64_t jlo, jhi;
+        shard(j, jlo, jhi);
+        const uint64_t lo = std::min(jhi, jlo + (uint64_t)p * cp * P.CH);
+        const uint64_t hi = std::min(jhi, jlo + (uint64_t)(p + 1) * cp * P.CH);
+        if (lo >= hi) continue;
+        uint8_t* dst = static_cast<uint8_t*>(a.rx[j]) + ((uint64_t)me * P.sl + (lo - jlo)) * esz;
+        uint64_t pb = 0;
+        for (int k = 0; k < a.g.n; ++k) {
+          const uint64_t pe = a.g.end[k], ol = std::max(lo, pb), oh = std::min(hi, pe);
+          if (ol < oh) {
+            e = cudaMemcpyAsync(dst + (ol - lo) * esz, static_cast<const uint8_t*>(a.g.p[k]) + (ol - pb) * esz,
+                                (oh - ol) * esz, cudaMemcpyDeviceToDevice, x->ce_rs);
+            if (e != cudaSuccess) return fail(PGX_E_CUDA, "peer copy: %s", cudaGetErrorString(e));
+          }
+          pb = pe;
+        }
+        fr.f[fr.k] = a.rxflags[j] + (uint64_t)me * P.C + (uint64_t)p * cp;
+        fr.n[fr.k++] = (uint32_t)((hi - lo + P.CH - 1) / P.CH);
+      }
+      if (!fr.k) continue;
+      xrecord(x->rs_part_ev[l][p], x->ce_rs);
+      xwait(x->ce_rs2, x->rs_part_ev[l][p]);
+      k_signal_range<<<1, 256, 0, x->ce_rs2>>>(fr, a.epoch, a.iter);
+      ++x->launches;
+    }
+    xrecord(x->rs_done[l], x->ce_rs);
+    xrecord(x->rs2_done[l], x->ce_rs2);
+  }
+  if (phases & PGX_PHASE_OWNER) {
+    xwait(x->ce_own, x->ready[l]);
+    uint64_t lo, hi;
+    shard(me, lo, hi);
+    const uint32_t mine = lo < hi ? (uint32_t)((hi - lo + P.CH - 1) / P.CH) : 0;
+    if (mine && N > 1) {  // the owner CTAs start once the first part has arrived from every peer
+      FlagSet fs{};
+      for (int sidx = 0; sidx < N; ++sidx)
+        if (sidx != me) fs.f[fs.n++] = a.rxflags[me] + (uint64_t)sidx * P.C + (std::min(cp, mine) - 1);
+      k_wait_flags<<<1, 32, 0, x->ce_own>>>(fs, a.epoch, a.iter, 1u, a.st);
+      ++x->launches;
+    }
+    a.item_begin = P.push_items;
+    a.item_end = P.items;
+    if (mine) {
+      ++x->launches;
+      launch_twoshot_bulk(N, (int)std::min<uint32_t>(mine, (uint32_t)P.grid), x->dev, x->ce_own, a);
+    }
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = xrecord(x->done[l], x->ce_own);
+    if (e != cudaSuccess) return fail(PGX_E_CUDA, "exchange launch failed: %s", cudaGetErrorString(e));
+  }
+  return PGX_OK;
+}
+
 extern "C" {
 
 int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
@@ -2412,6 +2492,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   x->auto_chunk_nvls = (cfg->flags & PGX_XF_NO_AUTO_CHUNK_NVLS) == 0;
   x->oneshot_small_chunks = (cfg->flags & PGX_XF_ONESHOT_SMALL_CHUNKS) != 0;
   x->tma = (cfg->flags & PGX_XF_TMA) != 0;
+  x->bulk_ce_rs = (cfg->flags & PGX_XF_BULK_CE_RS) != 0;
   x->ce_rs_parts = (cfg->flags & PGX_XF_CE_RS_PARTS) != 0;
   if (cfg->ce_parts) x->ce_parts = cfg->ce_parts;
   if (cfg->ce_rs_streams) x->ce_rs_streams = cfg->ce_rs_streams;
@@ -2866,6 +2947,11 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     return rc;
   }
   xrecord(x->ready[l], s);
+  if (P.variant == PGX_VARIANT_TWOSHOT_BULK && x->bulk_ce_rs && x->world > 1) {
+    const int rc = launch_bulk_ce_rs(x, l, P, a, phases);
+    if (prev != x->dev) cudaSetDevice(prev);
+    return rc;
+  }
   if (P.variant == PGX_VARIANT_TWOSHOT_BULK) {
     a.item_begin = (phases & PGX_PHASE_PUSH) ? 0 : P.push_items;
     a.item_end = (phases & PGX_PHASE_OWNER) ? P.items : P.push_items;

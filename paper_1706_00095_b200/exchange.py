@@ -26,10 +26,12 @@ from .errors import ConfigError, ShapeError
 VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot_ce": _lib.VARIANT_TWOSHOT_CE,
             "nvls": _lib.VARIANT_NVLS, "oneshot": _lib.VARIANT_ONESHOT, "twoshot_cep": _lib.VARIANT_TWOSHOT_CEP,
             "oneshot_ll": _lib.VARIANT_ONESHOT_LL, "oneshot_l128": _lib.VARIANT_ONESHOT_L128,
-            "twoshot_bulk": _lib.VARIANT_TWOSHOT_BULK, "twoshot_l128": _lib.VARIANT_TWOSHOT_L128}
+            "twoshot_bulk": _lib.VARIANT_TWOSHOT_BULK, "twoshot_l128": _lib.VARIANT_TWOSHOT_L128,
+            # TWOSHOT_BULK with its reduce-scatter on the copy engines (the bulk_ce_rs flag)
+            "twoshot_ceb": _lib.VARIANT_TWOSHOT_BULK}
 FLAGS = {"ce_rs_parts": _lib.XF_CE_RS_PARTS, "tma": _lib.XF_TMA, "oneshot_small_chunks": _lib.XF_ONESHOT_SMALL_CHUNKS,
          "auto_chunk_tree": _lib.XF_AUTO_CHUNK_TREE, "no_auto_chunk_nvls": _lib.XF_NO_AUTO_CHUNK_NVLS,
-         "allow_l128": _lib.XF_ALLOW_L128, "bulk_lean": _lib.XF_BULK_LEAN}
+         "allow_l128": _lib.XF_ALLOW_L128, "bulk_lean": _lib.XF_BULK_LEAN, "bulk_ce_rs": _lib.XF_BULK_CE_RS}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 
@@ -52,7 +54,9 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
     keeps the SM two-shot for the large layers too (run with a CTA cap and big chunks,
     see DeviceExchange `large_ctas`); large="cep" moves the reduce-scatter by copy engine
     and runs fold + update + all-gather as the SM owner kernel on a capped grid;
-    large="bulk" moves every byte with TMA bulk copies from a capped grid (TWOSHOT_BULK).
+    large="bulk" moves every byte with TMA bulk copies from a capped grid (TWOSHOT_BULK);
+    large="ceb" is TWOSHOT_BULK with the reduce-scatter on the copy engines (DeviceExchange
+    adds the bulk_ce_rs flag): the kernel only folds, updates and all-gathers.
     `l128_range` = [lo, hi) elements sent by the fence-free 128-byte-line two-shot
     (TWOSHOT_L128; DeviceExchange passes it only with the allow_l128 flag)."""
     if oneshot_below is None:  # one-shot moves (N-1)*S per GPU: the crossover shrinks with N
@@ -66,7 +70,8 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
     if world > 1 and elems < oneshot_below:
         return "oneshot"
     if world > 1 and elems >= ce_from:
-        return {"ce": "twoshot_ce", "cep": "twoshot_cep", "sm": "twoshot", "bulk": "twoshot_bulk"}[large]
+        return {"ce": "twoshot_ce", "cep": "twoshot_cep", "sm": "twoshot", "bulk": "twoshot_bulk",
+                "ceb": "twoshot_ceb"}[large]
     return "twoshot"
 
 
@@ -88,6 +93,7 @@ class DeviceExchange:
         defaults are the measured choices."""
         if mode not in MODES:
             raise ConfigError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
+        flags = tuple(flags)
         self.tr = transport
         self.world = transport.world_size
         self.rank = transport.rank
@@ -105,6 +111,11 @@ class DeviceExchange:
             variants = list(variant)
         if len(variants) != L or any(v not in VARIANTS for v in variants):
             raise ConfigError(f"bad variant list {variants}")
+        if "twoshot_ceb" in variants:  # one library flag switches every bulk layer's reduce-scatter
+            if "twoshot_bulk" in variants:
+                raise ConfigError("twoshot_bulk and twoshot_ceb layers cannot be mixed in one exchange")
+            if "bulk_ce_rs" not in flags:
+                flags += ("bulk_ce_rs",)
         self.variants = variants
         self.scale = 1.0 / self.world if scale is None else float(scale)
         self._elems = (C.c_uint64 * L)(*self.layer_elems)

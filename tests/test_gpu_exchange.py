@@ -38,7 +38,7 @@ def stepped_layer(xs, trs, l, k, pieces_by_rank, gate=True):
     N = len(xs)
     sync = torch.cuda.synchronize
     if xs[0].variants[l] in ("twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128",
-                            "twoshot_bulk"):
+                            "twoshot_bulk", "twoshot_ceb"):
         for r in range(N):
             xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
         sync()
@@ -73,7 +73,7 @@ def split_pieces(g, cut):
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128"])
+                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128", "twoshot_ceb"])
 @pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64", "sum32"])
 def test_exchange_matches_oracle(cuda, N, variant, mode):
     if variant in ("oneshot_ll", "oneshot_l128", "twoshot_l128") and mode == "ref64":
@@ -186,7 +186,7 @@ class _FixedGrad(torch.nn.Module):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "twoshot_bulk",
-                                     "twoshot_l128"])
+                                     "twoshot_l128", "twoshot_ceb"])
 @pytest.mark.parametrize("gate", ["layer", "model"])
 def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     """A captured training step (device iteration counter) applies exactly the oracle update."""
@@ -236,7 +236,7 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128"])
+                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128", "twoshot_ceb"])
 def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
     """Layers smaller than one vector per rank (empty owner shards), ragged tails and a
     piece boundary inside a vector, 8 ranks stepped on one GPU, ref32 bit-exact."""
@@ -349,4 +349,33 @@ def test_cuda_graph_multi_layer_single_gpu(cuda, gate):
     assert tr.device_status() == 0
     bind.remove()
     x.close()
+    world.close()
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+def test_ceb_part_major_reduce_scatter_matches_oracle(cuda, N):
+    """TWOSHOT_BULK with the copy-engine reduce-scatter (twoshot_ceb): a layer with enough
+    slabs per shard for every one of the part-major copies + per-part chunk signals, a ragged
+    [W][b] piece cut inside a part, three iterations, fast32 bit-exact."""
+    elems = [4099, 3_000_003]
+    world, trs, xs = build(N, elems, "fast32", "twoshot_ceb", lr=0.01, momentum=0.9, weight_decay=5e-4)
+    w = [O.seeded_fill(5 ^ l, n, 0.05).astype(np.float32) for l, n in enumerate(elems)]
+    v = [np.zeros(n, np.float32) for n in elems]
+    for x in xs:
+        for l in range(len(elems)):
+            x.layer_views[l].copy_(torch.from_numpy(w[l]))
+    torch.cuda.synchronize()
+    for k in range(3):
+        for l in reversed(range(len(elems))):
+            n = elems[l]
+            grads = [np.random.default_rng([r, l, k]).standard_normal(n, dtype=np.float32) * np.float32(1e-2)
+                     for r in range(N)]
+            pieces = [split_pieces(torch.from_numpy(g).cuda(), n - 1001) for g in grads]
+            stepped_layer(xs, trs, l, k, pieces)
+            w[l], v[l] = O.exchange_iteration(grads, w[l], 0.01, "fast32", state=v[l], scale=1.0 / N,
+                                              momentum=0.9, weight_decay=5e-4)
+            for r in range(N):
+                assert xs[r].layer_views[l].cpu().numpy().tobytes() == w[l].tobytes(), (N, k, l, r)
+    for x in xs:
+        x.close()
     world.close()
