@@ -29,6 +29,7 @@ VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot
             "twoshot_bulk": _lib.VARIANT_TWOSHOT_BULK, "twoshot_l128": _lib.VARIANT_TWOSHOT_L128,
             # TWOSHOT_BULK with its reduce-scatter on the copy engines (the bulk_ce_rs flag)
             "twoshot_ceb": _lib.VARIANT_TWOSHOT_BULK}
+VARIANT_ALIASES = {"twoshot_ceb": ("twoshot_bulk", "bulk_ce_rs")}  # Python name -> (library variant, flag)
 FLAGS = {"ce_rs_parts": _lib.XF_CE_RS_PARTS, "tma": _lib.XF_TMA, "oneshot_small_chunks": _lib.XF_ONESHOT_SMALL_CHUNKS,
          "auto_chunk_tree": _lib.XF_AUTO_CHUNK_TREE, "no_auto_chunk_nvls": _lib.XF_NO_AUTO_CHUNK_NVLS,
          "allow_l128": _lib.XF_ALLOW_L128, "bulk_lean": _lib.XF_BULK_LEAN, "bulk_ce_rs": _lib.XF_BULK_CE_RS}

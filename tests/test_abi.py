@@ -62,13 +62,19 @@ def test_header_constants_match_the_python_mirror():
     import re
 
     from paper_1706_00095_b200 import errors
-    from paper_1706_00095_b200.exchange import MODES, VARIANTS
+    from paper_1706_00095_b200.exchange import FLAGS, MODES, VARIANT_ALIASES, VARIANTS
 
     text = open(os.path.join(os.path.dirname(_lib.LIB_PATH), "..", "include", "pgx.h")).read()
     enum = {m.group(1): int(m.group(2)) for m in re.finditer(r"\b(PGX_[A-Z0-9_]+)\s*=\s*(\d+)", text)}
     define = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(PGX_[A-Z0-9_]+)\s+(\d+)", text)}
     for name, val in VARIANTS.items():
+        if name in VARIANT_ALIASES:  # a library variant run with a flag
+            base, flag = VARIANT_ALIASES[name]
+            assert VARIANTS[base] == val and flag in FLAGS, name
+            continue
         assert enum["PGX_VARIANT_" + name.upper()] == val, name
+    for name, val in FLAGS.items():
+        assert enum["PGX_XF_" + name.upper()] == val, name
     for name, val in MODES.items():
         assert enum["PGX_MODE_" + name.upper()] == val, name
     assert define["PGX_XCHG_STREAMS"] == _lib.XCHG_STREAMS
