@@ -158,7 +158,8 @@ int pgx_fold_update(int mode, const void* const* partials, int world, void* w, f
  * kernel from / into the layers (fp32 layers are promoted exactly / rounded to
  * nearest); header validation is host code with the reference's FormatError
  * messages. */
-#define PGX_CKPT_MAX_LAYERS 512
+#define PGX_CKPT_MAX_LAYERS 512  /* layers whose table travels as the kernel parameter; more
+                                    layers use a stream-ordered device copy (no format limit) */
 /* image bytes = 5 + sum(12 + 8*count) */
 int pgx_ckpt_image_bytes(const uint64_t* counts, int num_layers, uint64_t* bytes_out);
 /* Host: walk and validate a PSGD1 blob (load_model_bytes, checkpoint.py:42-63);

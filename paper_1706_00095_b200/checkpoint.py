@@ -74,8 +74,6 @@ def pack(layers, stream=None, out: torch.Tensor | None = None) -> tuple[torch.Te
     ts = _flat_layers(layers)
     if not ts:
         raise FormatError("checkpoint holds no layers")
-    if len(ts) > _lib.CKPT_MAX_LAYERS:
-        raise ConfigError(f"{len(ts)} layers > {_lib.CKPT_MAX_LAYERS} per checkpoint")
     dev = ts[0].device
     counts = [t.numel() for t in ts]
     nbytes = image_bytes(counts)

@@ -15,8 +15,10 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "pgx_common.cuh"
 
@@ -27,10 +29,20 @@ namespace {
 constexpr int kMaxLayers = PGX_CKPT_MAX_LAYERS;
 constexpr int kThreads = 256;
 
-struct CkptTable {                // kernel parameter (< 32 KB)
+struct CkptTable {                // kernel parameter (< 32 KB): up to kMaxLayers layers
   const void* p[kMaxLayers];      // layer data: source (pack) or destination (unpack)
   uint64_t off[kMaxLayers + 1];   // byte offset of layer l's header; off[L] = image bytes
   uint64_t cum[kMaxLayers + 1];   // cumulative element counts
+  int L;
+  int esz;
+};
+
+// The same table in device memory, for checkpoints of more layers (the PSGD1 format has no
+// layer limit, checkpoint.py:29-39); the kernels are templates over the two.
+struct CkptDevTable {
+  const void* const* p;
+  const uint64_t* off;
+  const uint64_t* cum;
   int L;
   int esz;
 };
@@ -48,12 +60,14 @@ __device__ __forceinline__ int find_layer(const uint64_t* a, int L, uint64_t x) 
   return lo;
 }
 
-__device__ __forceinline__ uint64_t value_bits(const CkptTable& t, int l, uint64_t k) {
+template <class Tab>
+__device__ __forceinline__ uint64_t value_bits(const Tab& t, int l, uint64_t k) {
   if (t.esz == 8) return (uint64_t)__double_as_longlong(static_cast<const double*>(t.p[l])[k]);
   return (uint64_t)__double_as_longlong((double)static_cast<const float*>(t.p[l])[k]);
 }
 
-__device__ uint8_t image_byte(const CkptTable& t, uint64_t pos) {
+template <class Tab>
+__device__ uint8_t image_byte(const Tab& t, uint64_t pos) {
   if (pos < 5) return (uint8_t)("PSGD1"[pos]);
   int l = find_layer(t.off, t.L, pos);
   uint64_t r = pos - t.off[l];
@@ -64,7 +78,8 @@ __device__ uint8_t image_byte(const CkptTable& t, uint64_t pos) {
 }
 
 // One thread = one aligned 16-byte output pair (one 128-bit store).
-__global__ void __launch_bounds__(kThreads) k_ckpt_pack(const __grid_constant__ CkptTable t, uint4* __restrict__ img,
+template <class Tab>
+__global__ void __launch_bounds__(kThreads) k_ckpt_pack(const __grid_constant__ Tab t, uint4* __restrict__ img,
                                                         uint64_t pairs) {
   const uint64_t bytes = t.off[t.L];
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < pairs; q += (uint64_t)gridDim.x * blockDim.x) {
@@ -99,7 +114,8 @@ __global__ void __launch_bounds__(kThreads) k_ckpt_pack(const __grid_constant__ 
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_ckpt_unpack(const __grid_constant__ CkptTable t,
+template <class Tab>
+__global__ void __launch_bounds__(kThreads) k_ckpt_unpack(const __grid_constant__ Tab t,
                                                           const uint64_t* __restrict__ img) {
   const uint64_t total = t.cum[t.L];
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -115,6 +131,45 @@ __global__ void __launch_bounds__(kThreads) k_ckpt_unpack(const __grid_constant_
     else
       static_cast<float*>(const_cast<void*>(t.p[l]))[k] = __double2float_rn(v);
   }
+}
+
+// Host copy of a table of any size: per-layer pointers, header offsets, cumulative counts.
+struct HostTable {
+  std::vector<const void*> p;
+  std::vector<uint64_t> off, cum;
+};
+
+int build_host_table(HostTable& h, const void* const* layers, const uint64_t* counts, int L, int esz) {
+  if (L < 0) return fail(PGX_E_CONFIG, "negative checkpoint layer count %d", L);
+  if (esz != 4 && esz != 8) return fail(PGX_E_CONFIG, "element size %d is not 4 or 8", esz);
+  h.p.assign(std::max(L, 1), nullptr);
+  h.off.assign(L + 1, 5);
+  h.cum.assign(L + 1, 0);
+  for (int l = 0; l < L; ++l) {
+    if (counts[l] && !layers[l]) return fail(PGX_E_INPUT, "layer %d has no data pointer", l);
+    h.p[l] = layers[l];
+    h.off[l + 1] = h.off[l] + 12 + 8 * counts[l];
+    h.cum[l + 1] = h.cum[l] + counts[l];
+  }
+  return PGX_OK;
+}
+
+// Stream-ordered device copy of a large table: [p | off | cum] in one allocation, freed
+// behind the launch on the same stream.
+int upload_table(const HostTable& h, int L, int esz, cudaStream_t s, CkptDevTable* out, void** mem) {
+  const size_t np = h.p.size() * sizeof(void*), no = h.off.size() * sizeof(uint64_t);
+  std::vector<uint8_t> buf(np + 2 * no);
+  memcpy(buf.data(), h.p.data(), np);
+  memcpy(buf.data() + np, h.off.data(), no);
+  memcpy(buf.data() + np + no, h.cum.data(), no);
+  cudaError_t e = cudaMallocAsync(mem, buf.size(), s);
+  // pageable source: the copy is staged before cudaMemcpyAsync returns, so `buf` may go
+  if (e == cudaSuccess) e = cudaMemcpyAsync(*mem, buf.data(), buf.size(), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "checkpoint table upload: %s", cudaGetErrorString(e));
+  uint8_t* d = static_cast<uint8_t*>(*mem);
+  *out = {reinterpret_cast<const void* const*>(d), reinterpret_cast<const uint64_t*>(d + np),
+          reinterpret_cast<const uint64_t*>(d + np + no), L, esz};
+  return PGX_OK;
 }
 
 int build_table(CkptTable& t, const void* const* layers, const uint64_t* counts, int L, int esz) {
@@ -214,33 +269,61 @@ int pgx_ckpt_parse(const void* blob, uint64_t bytes, uint64_t* counts_out, int c
 
 int pgx_ckpt_pack(const void* const* layers, const uint64_t* counts, int num_layers, int elem_size, void* image,
                   uint64_t capacity, void* stream) {
-  std::unique_ptr<CkptTable> tp(new CkptTable());  // 12 KB; the launch copies it
-  CkptTable& t = *tp;
-  int rc = build_table(t, layers, counts, num_layers, elem_size);
+  HostTable h;
+  int rc = build_host_table(h, layers, counts, num_layers, elem_size);
   if (rc) return rc;
-  const uint64_t bytes = t.off[num_layers], pairs = (bytes + 15) / 16;
+  const uint64_t bytes = h.off[num_layers], pairs = (bytes + 15) / 16;
   if (capacity < pairs * 16) return fail(PGX_E_RANGE, "image buffer %llu bytes < %llu", (unsigned long long)capacity,
                                          (unsigned long long)(pairs * 16));
   if (reinterpret_cast<uintptr_t>(image) & 15) return fail(PGX_E_INPUT, "image buffer is not 16-byte aligned");
-  k_ckpt_pack<<<grid_for(pairs), kThreads, 0, (cudaStream_t)stream>>>(t, static_cast<uint4*>(image), pairs);
-  PGX_LAUNCH_CHECK();
+  cudaStream_t s = (cudaStream_t)stream;
+  if (num_layers <= kMaxLayers) {  // the table travels as the kernel parameter
+    std::unique_ptr<CkptTable> tp(new CkptTable());  // 12 KB; the launch copies it
+    rc = build_table(*tp, layers, counts, num_layers, elem_size);
+    if (rc) return rc;
+    k_ckpt_pack<CkptTable><<<grid_for(pairs), kThreads, 0, s>>>(*tp, static_cast<uint4*>(image), pairs);
+    PGX_LAUNCH_CHECK();
+    return PGX_OK;
+  }
+  CkptDevTable d;
+  void* mem = nullptr;
+  rc = upload_table(h, num_layers, elem_size, s, &d, &mem);
+  if (rc) return rc;
+  k_ckpt_pack<CkptDevTable><<<grid_for(pairs), kThreads, 0, s>>>(d, static_cast<uint4*>(image), pairs);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(mem, s);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return PGX_OK;
 }
 
 int pgx_ckpt_unpack(const void* image, uint64_t capacity, const uint64_t* counts, int num_layers, int elem_size,
                     void* const* layers, void* stream) {
-  std::unique_ptr<CkptTable> tp(new CkptTable());
-  CkptTable& t = *tp;
-  int rc = build_table(t, const_cast<const void* const*>(layers), counts, num_layers, elem_size);
+  HostTable h;
+  int rc = build_host_table(h, const_cast<const void* const*>(layers), counts, num_layers, elem_size);
   if (rc) return rc;
-  const uint64_t need = (t.off[num_layers] + 7) / 8 * 8 + 8;  // the last value reads one word past its own
+  const uint64_t need = (h.off[num_layers] + 7) / 8 * 8 + 8;  // the last value reads one word past its own
   if (capacity < need) return fail(PGX_E_RANGE, "image buffer %llu bytes < %llu", (unsigned long long)capacity,
                                    (unsigned long long)need);
   if (reinterpret_cast<uintptr_t>(image) & 7) return fail(PGX_E_INPUT, "image buffer is not 8-byte aligned");
-  if (t.cum[num_layers] == 0) return PGX_OK;
-  k_ckpt_unpack<<<grid_for(t.cum[num_layers]), kThreads, 0, (cudaStream_t)stream>>>(
-      t, static_cast<const uint64_t*>(image));
-  PGX_LAUNCH_CHECK();
+  if (h.cum[num_layers] == 0) return PGX_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t total = h.cum[num_layers];
+  if (num_layers <= kMaxLayers) {
+    std::unique_ptr<CkptTable> tp(new CkptTable());
+    rc = build_table(*tp, const_cast<const void* const*>(layers), counts, num_layers, elem_size);
+    if (rc) return rc;
+    k_ckpt_unpack<CkptTable><<<grid_for(total), kThreads, 0, s>>>(*tp, static_cast<const uint64_t*>(image));
+    PGX_LAUNCH_CHECK();
+    return PGX_OK;
+  }
+  CkptDevTable d;
+  void* mem = nullptr;
+  rc = upload_table(h, num_layers, elem_size, s, &d, &mem);
+  if (rc) return rc;
+  k_ckpt_unpack<CkptDevTable><<<grid_for(total), kThreads, 0, s>>>(d, static_cast<const uint64_t*>(image));
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(mem, s);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
   return PGX_OK;
 }
 

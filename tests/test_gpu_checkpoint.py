@@ -70,10 +70,12 @@ def test_load_errors(case):
     assert str(ei.value) == M["ckpt_errors"][case]
 
 
-@pytest.mark.parametrize("sizes", [[0, 1, 5, 0, 3], [1], [7, 0], ALEXNET])
+@pytest.mark.parametrize("sizes", [[0, 1, 5, 0, 3], [1], [7, 0], ALEXNET, [(i * 7) % 34 for i in range(700)]])
 def test_ragged_and_full_size_roundtrip(sizes, tmp_path):
-    """Ragged / empty layers and the full AlexNet model (fp32 as the exchange holds it):
-    bytes equal the oracle's image, and loading them back is the identity."""
+    """Ragged / empty layers, the full AlexNet model (fp32 as the exchange holds it) and a
+    700-layer model (more layers than the kernel-parameter table holds: the table goes
+    through device memory; the format has no layer limit): bytes equal the oracle's image,
+    and loading them back is the identity."""
     from paper_1706_00095_b200.checkpoint import load_model, save_model
 
     g = torch.Generator(device="cuda").manual_seed(1706)
