@@ -127,6 +127,43 @@ __device__ __forceinline__ void grad_vec(const Pieces& P, uint64_t e, int cnt, T
   }
 }
 
+// The gradient of [lo, hi) when it lies in ONE piece at a 16-byte aligned address (the
+// common case: only the slab holding the [W][b] boundary straddles pieces), else null.
+// Owner loops resolve it once per slab instead of searching the piece table (dynamically
+// indexed kernel parameters: LDC + short-scoreboard waits) for every vector.
+template <class T>
+__device__ __forceinline__ const T* slab_grad(const Pieces& P, uint64_t lo, uint64_t hi) {
+  uint64_t pb = 0;
+  for (int k = 0; k < P.n; ++k) {
+    const uint64_t pe = P.end[k];
+    if (lo >= pb && hi <= pe) {
+      const T* g = static_cast<const T*>(P.p[k]) + (lo - pb);
+      return (reinterpret_cast<uintptr_t>(g) & 15) ? nullptr : g;
+    }
+    pb = pe;
+  }
+  return nullptr;
+}
+
+// W gradient elements at logical element e: from the resolved slab pointer (gs = element
+// lo) when there is one, else through the piece table.
+template <class T>
+__device__ __forceinline__ void grad_vec_slab(const T* gs, const Pieces& P, uint64_t lo, uint64_t e, int cnt, T* out) {
+  constexpr int W = VecT<T>::W;
+  if (gs) {
+    const T* src = gs + (e - lo);
+    if (cnt == W) {
+      typename VecT<T>::V v = __ldcs(reinterpret_cast<const typename VecT<T>::V*>(src));
+      memcpy(out, &v, sizeof(v));
+    } else {
+#pragma unroll
+      for (int i = 0; i < W; ++i) out[i] = i < cnt ? src[i] : T(0);
+    }
+  } else {
+    grad_vec<T>(P, e, cnt, out);
+  }
+}
+
 template <class T>
 __device__ __forceinline__ void ld_vec(const T* p, int cnt, T* out) {
   constexpr int W = VecT<T>::W;
@@ -192,7 +229,7 @@ __device__ __forceinline__ void update_vec(T* w, const T* g, float* v, int cnt, 
 // tile != nullptr: also stage it in shared memory for TMA bulk stores.
 template <int N, class T, int U, bool kRemote = true>
 __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint64_t lo, uint64_t hi,
-                                              uint64_t q0, uint64_t nvec, T* tile = nullptr) {
+                                              uint64_t q0, uint64_t nvec, T* tile = nullptr, const T* gs = nullptr) {
   constexpr int W = VecT<T>::W;
   const int me = a.rank;
   const bool fast = sizeof(T) == 4 && a.mode == PGX_MODE_FAST32;
@@ -209,7 +246,7 @@ __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint
 #pragma unroll
       for (int s = 0; s < N; ++s) {
         if (s == me)
-          grad_vec<T>(a.g, e, cnt[u], vals[u][s]);
+          grad_vec_slab<T>(gs, a.g, lo, e, cnt[u], vals[u][s]);
         else
           ld_vec<T>(rxb + (uint64_t)s * a.sl + q * W, cnt[u], vals[u][s]);
       }
@@ -410,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
         T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + (lo - j * a.sl));
         uint64_t nvec = (hi - lo + W - 1) / W;
         constexpr int UP = 4;
+        const T* gs = slab_grad<T>(a.g, lo, hi);
         for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)UP * blockDim.x) {
           T buf[UP][W];
           int cnt[UP];
@@ -418,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
             uint64_t q = q0 + (uint64_t)u * blockDim.x;
             uint64_t e = lo + q * W;
             cnt[u] = q < nvec ? (int)min((uint64_t)W, hi - e) : 0;
-            if (cnt[u] > 0) grad_vec<T>(a.g, e, cnt[u], buf[u]);
+            if (cnt[u] > 0) grad_vec_slab<T>(gs, a.g, lo, e, cnt[u], buf[u]);
           }
 #pragma unroll
           for (int u = 0; u < UP; ++u)
@@ -441,10 +479,11 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
       const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl + (lo - me * a.sl);
       uint64_t nvec = (hi - lo + W - 1) / W;
       constexpr int U = N <= 2 ? 2 : 1;  // 2 CTAs/SM (64 regs) without spills
+      const T* gs = slab_grad<T>(a.g, lo, hi);
       if constexpr (kTma) {
         T* tile = reinterpret_cast<T*>(tma_buf);
         for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
-          owner_vectors<N, T, U, false>(a, rxb, lo, hi, q0, nvec, tile);
+          owner_vectors<N, T, U, false>(a, rxb, lo, hi, q0, nvec, tile, gs);
         __syncthreads();
         if (threadIdx.x == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
@@ -466,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, (N <= 4 && !kTma) ? 2 : 1) k_twoshot
         __syncthreads();  // the tile is reused by the next item
       } else {
         for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)U * blockDim.x)
-          owner_vectors<N, T, U>(a, rxb, lo, hi, q0, nvec);
+          owner_vectors<N, T, U>(a, rxb, lo, hi, q0, nvec, nullptr, gs);
         __syncthreads();
         if (threadIdx.x < N - 1) {
           int s = threadIdx.x + (threadIdx.x >= (unsigned)me);
@@ -694,6 +733,7 @@ __global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XAr
       trace_stamp(a, it, 1);
       const T* rx0 = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl - (uint64_t)me * a.sl;
       T* wme = static_cast<T*>(a.model[me]);
+      const T* gs = slab_grad<T>(a.g, lo, hi);
       constexpr int U = N <= 4 ? 4 : 2;                         // vectors per thread per round
       const uint64_t RE = (uint64_t)blockDim.x * U * W;         // elements per round
       const int K = (int)(G::kRing / (RE * sizeof(T)));         // output ring slots
@@ -715,7 +755,7 @@ __global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XAr
 #pragma unroll
             for (int s = 0; s < N; ++s) {
               if (s == me)
-                grad_vec<T>(a.g, e, cnt[u], vals[u][s]);
+                grad_vec_slab<T>(gs, a.g, lo, e, cnt[u], vals[u][s]);
               else
                 ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt[u], vals[u][s]);
             }
@@ -809,11 +849,12 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && N >= 3 && N <= 4)
       uint64_t lo = (uint64_t)c * a.CH, hi = min(lo + a.CH, a.S);
       T* dst = static_cast<T*>(a.rx[j]) + ((uint64_t)(parity * a.K + me) * a.sl + lo);
       uint64_t nvec = (hi - lo + W - 1) / W;
+      const T* gs = slab_grad<T>(a.g, lo, hi);
       for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
         uint64_t e = lo + q * W;
         int cnt = (int)min((uint64_t)W, hi - e);
         T buf[W];
-        grad_vec<T>(a.g, e, cnt, buf);
+        grad_vec_slab<T>(gs, a.g, lo, e, cnt, buf);
         st_vec<T>(dst + q * W, cnt, buf);
       }
       trace_stamp(a, it, 1);
@@ -834,8 +875,9 @@ __global__ void __launch_bounds__(kThreads, (sizeof(T) == 4 && N >= 3 && N <= 4)
       // fp32 and N <= 4: two vectors per thread in flight (the fold is load-latency bound;
       // profiles/r4i: 8 us of a 1 MB exchange at N=4 with one)
       constexpr int UO = (sizeof(T) == 4 && N <= 4) ? 2 : 1;
+      const T* gs = slab_grad<T>(a.g, lo, hi);
       for (uint64_t q0 = threadIdx.x; q0 < nvec; q0 += (uint64_t)UO * blockDim.x)
-        owner_vectors<N, T, UO, false>(a, rxb, lo, hi, q0, nvec);
+        owner_vectors<N, T, UO, false>(a, rxb, lo, hi, q0, nvec, nullptr, gs);
       __syncthreads();
       trace_stamp(a, it, 2);
     }
@@ -1311,11 +1353,12 @@ __global__ void __launch_bounds__(kThreads) k_tree_up(XArgs a) {
     cta_wait_flags(s_flags, nc, epoch, a.st);
     const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl;
     uint64_t nvec = (hi - lo + W - 1) / W;
+    const T* gs = slab_grad<T>(a.g, lo, hi);
     for (uint64_t q = threadIdx.x; q < nvec; q += blockDim.x) {
       uint64_t e = lo + q * W;
       int cnt = (int)min((uint64_t)W, hi - e);
       T acc[W];
-      grad_vec<T>(a.g, e, cnt, acc);
+      grad_vec_slab<T>(gs, a.g, lo, e, cnt, acc);
       for (int s = 0; s < nc; ++s) {
         T x[W];
         ld_vec<T>(rxb + (uint64_t)s * a.sl + e, cnt, x);
@@ -1623,8 +1666,9 @@ __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
   // receive slots are indexed from the shard start; owner_vectors indexes them by q
   const T* rxb = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl + (lo - base);
   const uint64_t nvec = (hi - lo + W - 1) / W, span = (uint64_t)U * blockDim.x;
+  const T* gs = slab_grad<T>(a.g, lo, hi);
   for (uint64_t blk = blockIdx.x; blk * span < nvec; blk += gridDim.x)
-    owner_vectors<N, T, U, false>(a, rxb, lo, hi, blk * span + threadIdx.x, nvec);
+    owner_vectors<N, T, U, false>(a, rxb, lo, hi, blk * span + threadIdx.x, nvec, nullptr, gs);
 }
 
 constexpr int kCepCtas = 48;  // TWOSHOT_CEP owner grid default

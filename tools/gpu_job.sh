@@ -1,22 +1,32 @@
 #!/bin/bash
-# r5x (4 GPUs): TWOSHOT_BULK with the copy-engine reduce-scatter (twoshot_ceb): parity
-# (stepped 1 GPU, concurrent 4 GPUs), sweep vs the copy-engine and bulk variants, in-step AlexNet.
+# r5y (4 GPUs): gradient pointer resolved once per slab in every owner / push loop
+# (slab_grad): the 1-GPU suite, ncu of the stepped bulk / two-shot kernels (compare r5t),
+# N=1 bench, N=4 sweep of the large layers and in-step AlexNet (ce default vs bulk 48).
 cd "$(dirname "$0")/.." || exit 1
 O=gpurun_out
 mkdir -p $O
-CUDA_VISIBLE_DEVICES=0 timeout 900 python -m pytest tests/test_gpu_exchange.py -m gpu -q -x -k "ceb" > $O/r5x_pytest_ceb_1gpu.log 2>&1; echo "stepped rc=$?"
-timeout 900 python -m pytest tests/test_gpu_multi.py -m gpu -q -rA -k "ceb" > $O/r5x_pytest_ceb_4gpus.log 2>&1; echo "multi rc=$?"
-for c in 24 48; do
-  timeout 600 torchrun --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 297$c \
-    tools/sweep.py --min-kb 16384 --max-mb 256 --ctas $c --variants twoshot_ceb,twoshot_bulk > $O/r5x_sweep_n4_c$c.jsonl 2> $O/r5x_sweep_n4_c$c.err
-  echo "sweep c=$c rc=$?"
-done
+CUDA_VISIBLE_DEVICES=0 timeout 1200 python -m pytest tests -m gpu -x -q > $O/r5y_pytest_gpu_1gpu.log 2>&1; echo "suite rc=$?"
+FC6=37752832
+run() {  # name variants regex skip count
+  local name=$1 var=$2 rx=$3 sk=$4 cnt=$5
+  local cmd="python tools/ncu_stepped.py --world 4 --elems $FC6 --variants $var --iters 2"
+  CUDA_VISIBLE_DEVICES=0 timeout 300 $cmd > $O/r5y_plain_$name.log 2>&1 && \
+  CUDA_VISIBLE_DEVICES=0 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k regex:"$rx" -s $sk -c $cnt -o $O/r5y_ncu_$name $cmd > $O/r5y_ncu_$name.log 2>&1
+  echo "ncu $name rc=$?"
+  ncu -i $O/r5y_ncu_$name.ncu-rep --page raw --csv > $O/r5y_ncu_${name}_raw.csv 2>/dev/null
+  ncu -i $O/r5y_ncu_$name.ncu-rep --page details --csv > $O/r5y_ncu_${name}_details.csv 2>/dev/null
+  rm -f $O/r5y_ncu_$name.ncu-rep
+}
+run twoshot4 twoshot "k_twoshot<.int.4," 8 5
+run bulk4 twoshot_bulk "k_twoshot_bulk<.int.4," 8 5
+CUDA_VISIBLE_DEVICES=0 timeout 900 python bench.py > $O/r5y_bench1.json 2> $O/r5y_bench1.err; echo "b1 rc=$?"
+timeout 600 torchrun --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29761 tools/sweep.py --min-kb 16384 --max-mb 256 \
+  --variants twoshot,twoshot_ce > $O/r5y_sweep_n4.jsonl 2> $O/r5y_sweep_n4.err; echo "sweep rc=$?"
+timeout 600 torchrun --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29762 tools/sweep.py --min-kb 16384 --max-mb 256 \
+  --ctas 48 --variants twoshot_bulk > $O/r5y_sweep_n4_bulk48.jsonl 2> $O/r5y_sweep_n4_bulk48.err; echo "sweep48 rc=$?"
 TR="torchrun --nproc-per-node 4 --master-addr 127.0.0.1"
 B="bench.py --gpus 4 --steps 30 --warmup 5 --no-cpu-baseline"
-timeout 900 $TR --master-port 29851 $B > $O/r5x_bench4_ce.json 2> $O/r5x_bench4_ce.err; echo "b0 rc=$?"
-timeout 900 $TR --master-port 29852 $B --large ceb --large-ctas 24 > $O/r5x_bench4_ceb24.json 2> $O/r5x_bench4_ceb24.err; echo "b1 rc=$?"
-timeout 900 $TR --master-port 29853 $B --large ceb --large-ctas 48 > $O/r5x_bench4_ceb48.json 2> $O/r5x_bench4_ceb48.err; echo "b2 rc=$?"
-timeout 900 $TR --master-port 29854 $B --large ceb --large-ctas 24 --xflags bulk_lean > $O/r5x_bench4_ceb24_lean.json 2> $O/r5x_bench4_ceb24_lean.err; echo "b3 rc=$?"
-timeout 900 $TR --master-port 29855 $B --large ceb --large-ctas 48 --xflags bulk_lean > $O/r5x_bench4_ceb48_lean.json 2> $O/r5x_bench4_ceb48_lean.err; echo "b4 rc=$?"
-timeout 900 $TR --master-port 29856 $B > $O/r5x_bench4_ce_b.json 2> $O/r5x_bench4_ce_b.err; echo "b5 rc=$?"
+timeout 900 $TR --master-port 29863 $B > $O/r5y_bench4.json 2> $O/r5y_bench4.err; echo "b4 rc=$?"
+timeout 900 $TR --master-port 29864 $B --large bulk --large-ctas 48 > $O/r5y_bench4_bulk48.json 2> $O/r5y_bench4_bulk48.err; echo "b4bulk rc=$?"
 echo done
