@@ -379,3 +379,43 @@ def test_ceb_part_major_reduce_scatter_matches_oracle(cuda, N):
     for x in xs:
         x.close()
     world.close()
+
+
+@pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "oneshot", "oneshot_ll", "twoshot_bulk",
+                                     "twoshot_l128", "twoshot_ceb"])
+def test_misaligned_gradient_views_match_oracle(cuda, variant):
+    """Gradient pieces that are views at 4- and 12-byte offsets into larger buffers (not
+    16-byte aligned): the kernels must fall back from the per-slab vector path to the
+    element-wise piece lookup and stay bit-exact (N=4, fast32, a slab-straddling cut)."""
+    N = 4
+    elems = [70001, 1_200_007]
+    world, trs, xs = build(N, elems, "fast32", variant, lr=0.01, momentum=0.9, weight_decay=5e-4)
+    w = [O.seeded_fill(11 ^ l, n, 0.05).astype(np.float32) for l, n in enumerate(elems)]
+    v = [np.zeros(n, np.float32) for n in elems]
+    for x in xs:
+        for l in range(len(elems)):
+            x.layer_views[l].copy_(torch.from_numpy(w[l]))
+    torch.cuda.synchronize()
+    keep = []
+    for k in range(2):
+        for l in reversed(range(len(elems))):
+            n = elems[l]
+            grads = [np.random.default_rng([r, l, k, 3]).standard_normal(n, dtype=np.float32) * np.float32(1e-2)
+                     for r in range(N)]
+            cut = n // 2 + 1
+            pieces = []
+            for g in grads:
+                a = torch.zeros(cut + 8, device="cuda")
+                b = torch.zeros(n - cut + 8, device="cuda")
+                a[1:1 + cut] = torch.from_numpy(g[:cut]).cuda()
+                b[3:3 + n - cut] = torch.from_numpy(g[cut:]).cuda()
+                pieces.append([a[1:1 + cut], b[3:3 + n - cut]])
+                keep += [a, b]
+            stepped_layer(xs, trs, l, k, pieces)
+            w[l], v[l] = O.exchange_iteration(grads, w[l], 0.01, "fast32", state=v[l], scale=1.0 / N,
+                                              momentum=0.9, weight_decay=5e-4)
+            for r in range(N):
+                assert xs[r].layer_views[l].cpu().numpy().tobytes() == w[l].tobytes(), (variant, k, l, r)
+    for x in xs:
+        x.close()
+    world.close()
