@@ -237,6 +237,35 @@ __device__ __forceinline__ void owner_vectors(const XArgs& a, const T* rxb, uint
   T w[U][W];
   float vv[U][W];
   int cnt[U];
+  if (gs != nullptr && lo + (q0 + (uint64_t)(U - 1) * blockDim.x + 1) * W <= hi) {
+    // every vector of this call is whole: straight-line code, all U*(N+2) loads in flight
+    // before the first use (the per-vector count / piece checks serialised them)
+    using V = typename VecT<T>::V;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t q = q0 + (uint64_t)u * blockDim.x, e = lo + q * W;
+      cnt[u] = W;
+#pragma unroll
+      for (int s = 0; s < N; ++s) {
+        const T* src = (s == me) ? gs + (e - lo) : rxb + (uint64_t)s * a.sl + q * W;
+        const V x = __ldcg(reinterpret_cast<const V*>(src));
+        memcpy(vals[u][s], &x, sizeof(x));
+      }
+      if (a.mode != PGX_MODE_SUM32) {
+        const V x = __ldcg(reinterpret_cast<const V*>(static_cast<const T*>(a.model[me]) + e));
+        memcpy(w[u], &x, sizeof(x));
+      } else {
+#pragma unroll
+        for (int k = 0; k < W; ++k) w[u][k] = T(0);
+      }
+      if constexpr (sizeof(T) == 4) {
+        if (fast) {
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(a.v + e));
+          memcpy(vv[u], &x, sizeof(x));
+        }
+      }
+    }
+  } else
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     uint64_t q = q0 + (uint64_t)u * blockDim.x;
@@ -747,20 +776,46 @@ __global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XAr
         T vals[U][N][W], w[U][W];
         float vv[U][W];
         int cnt[U];
+        if (gs != nullptr && t1 - t0 == RE) {
+          // full round (every slab but a ragged last one): straight-line code, all U*(N+2)
+          // 16-byte loads issued before the first use — no per-vector count checks or
+          // piece lookups between them (those branches serialised the loads, ncu r5t/r5y)
+          using V = typename VecT<T>::V;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {  // every load of the round first
-          const uint64_t e = t0 + ((uint64_t)u * blockDim.x + threadIdx.x) * W;
-          cnt[u] = e < t1 ? (int)min((uint64_t)W, t1 - e) : 0;
-          if (cnt[u] > 0) {
+          for (int u = 0; u < U; ++u) {
+            const uint64_t e = t0 + ((uint64_t)u * blockDim.x + threadIdx.x) * W;
+            cnt[u] = W;
 #pragma unroll
             for (int s = 0; s < N; ++s) {
-              if (s == me)
-                grad_vec_slab<T>(gs, a.g, lo, e, cnt[u], vals[u][s]);
-              else
-                ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt[u], vals[u][s]);
+              const T* src = (s == me) ? gs + (e - lo) : rx0 + (uint64_t)s * a.sl + e;
+              const V x = __ldcg(reinterpret_cast<const V*>(src));
+              memcpy(vals[u][s], &x, sizeof(x));
             }
-            if constexpr (upd) ld_vec<T>(wme + e, cnt[u], w[u]);
-            if constexpr (fast) ld_vec<float>(a.v + e, cnt[u], vv[u]);
+            if constexpr (upd) {
+              const V x = __ldcg(reinterpret_cast<const V*>(wme + e));
+              memcpy(w[u], &x, sizeof(x));
+            }
+            if constexpr (fast) {
+              const float4 x = __ldcg(reinterpret_cast<const float4*>(a.v + e));
+              memcpy(vv[u], &x, sizeof(x));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {  // every load of the round first
+            const uint64_t e = t0 + ((uint64_t)u * blockDim.x + threadIdx.x) * W;
+            cnt[u] = e < t1 ? (int)min((uint64_t)W, t1 - e) : 0;
+            if (cnt[u] > 0) {
+#pragma unroll
+              for (int s = 0; s < N; ++s) {
+                if (s == me)
+                  grad_vec_slab<T>(gs, a.g, lo, e, cnt[u], vals[u][s]);
+                else
+                  ld_vec<T>(rx0 + (uint64_t)s * a.sl + e, cnt[u], vals[u][s]);
+              }
+              if constexpr (upd) ld_vec<T>(wme + e, cnt[u], w[u]);
+              if constexpr (fast) ld_vec<float>(a.v + e, cnt[u], vv[u]);
+            }
           }
         }
 #pragma unroll
