@@ -663,6 +663,134 @@ __device__ __forceinline__ T bulk_update(T w, T g, float& v, double lr, float sc
   }
 }
 
+// Owner fold fed by TMA loads.  The LSU path (one 16-byte load per thread and stream)
+// keeps ~48 KB in flight per SM and was lg_throttle-bound at ~39 GB/s per SM (ncu r5z:
+// the 24-CTA owner phase of fc6 ran 395 us); bulk loads keep SO-1 whole tiles of all
+// N + 2 input streams (N partials, w, v) in flight per CTA with no LSU slots at all.
+// Per tile: one elected thread issues the N + 2 cp.async.bulk loads onto the stage's
+// mbarrier; every thread folds its vectors from shared memory in tree order, applies
+// the fused update and writes w / v back IN PLACE; the elected thread then bulk-stores
+// the w tile into the local and every peer's weights and the v tile into the local
+// momentum.  A stage is reloaded only after wait_group.read says its stores have read it.
+template <int N, bool LEAN>
+struct OwnerGeo {
+  static constexpr int kTile = LEAN ? (N <= 4 ? 4096 : 2048) : (N <= 4 ? 8192 : 4096);  // bytes per stream
+  static constexpr int kStage = (N + 2) * kTile;
+  static constexpr int kStages0 = BulkGeo<LEAN>::kRing / kStage;
+  static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
+};
+
+// Folds [lo, lo + body) of the owner slab (body: the 16-byte-granular prefix) through the
+// TMA pipeline; returns the first element NOT done (lo when the slab is not eligible).
+// `ouse` counts the tiles this CTA ever consumed (mbarrier phases), identical in all threads.
+template <int N, class T, int MODE, bool LEAN>
+__device__ __forceinline__ uint64_t owner_tma(const XArgs& a, const T* rx0, const T* gs, uint64_t lo, uint64_t hi,
+                                              uint8_t* ring, uint64_t* obars, uint32_t& ouse) {
+  using OG = OwnerGeo<N, LEAN>;
+  constexpr int SO = OG::kStages;
+  constexpr int TB = OG::kTile;
+  constexpr int TE = TB / (int)sizeof(T);
+  constexpr bool fast = MODE == PGX_MODE_FAST32;
+  constexpr bool upd = MODE != PGX_MODE_SUM32;
+  if constexpr (SO < 2) {
+    return lo;
+  } else {
+    const int me = a.rank;
+    T* wme = static_cast<T*>(a.model[me]);
+    if (gs == nullptr) return lo;
+    uintptr_t al = reinterpret_cast<uintptr_t>(wme + lo);
+    if (fast) al |= reinterpret_cast<uintptr_t>(a.v + lo);
+    for (int s = 0; s < N; ++s)
+      if (s != me) al |= reinterpret_cast<uintptr_t>(rx0 + (uint64_t)s * a.sl + lo);
+    for (int d = 1; d < N; ++d) al |= reinterpret_cast<uintptr_t>(static_cast<T*>(a.model[(me + d) % N]) + lo);
+    if (al & 15) return lo;
+    const uint64_t body = (((hi - lo) * sizeof(T)) & ~uint64_t(15)) / sizeof(T);
+    const uint32_t nt = (uint32_t)((body + TE - 1) / TE);
+    if (nt == 0) return lo;
+    constexpr uint32_t nstream = N + (upd ? 1 : 0) + (fast ? 1 : 0);
+    auto issue = [&](uint32_t i) {  // tile i of the slab -> stage (ouse + i) % SO
+      const uint64_t e0 = lo + (uint64_t)i * TE;
+      const uint32_t nb = (uint32_t)(min((uint64_t)TE, lo + body - e0) * sizeof(T));
+      const uint32_t st = (ouse + i) % SO;
+      uint8_t* stage = ring + (size_t)st * OG::kStage;
+      mbar_expect_tx(&obars[st], nb * nstream);
+#pragma unroll
+      for (int s = 0; s < N; ++s)
+        tma_load(stage + s * TB, (s == me) ? gs + (e0 - lo) : rx0 + (uint64_t)s * a.sl + e0, nb, &obars[st]);
+      if constexpr (upd) tma_load(stage + N * TB, wme + e0, nb, &obars[st]);
+      if constexpr (fast) tma_load(stage + (N + 1) * TB, a.v + e0, nb, &obars[st]);
+    };
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired rx data -> async-proxy reads
+      for (uint32_t i = 0; i < min(nt, (uint32_t)SO - 1); ++i) issue(i);
+    }
+    using V = typename VecT<T>::V;
+    constexpr int W = VecT<T>::W;
+    const double lr = a.lr;
+    const float scale = a.scale, mu = a.mu, wd = a.wd;
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t g = ouse + t, st = g % SO;
+      const uint64_t e0 = lo + (uint64_t)t * TE;
+      const uint32_t nb = (uint32_t)(min((uint64_t)TE, lo + body - e0) * sizeof(T));
+      uint8_t* stage = ring + (size_t)st * OG::kStage;
+      mbar_wait(&obars[st], (g / SO) & 1u);
+      for (uint32_t q = threadIdx.x; q < nb / 16; q += blockDim.x) {
+        T vals[N][W], w[W];
+        float vv[W];
+#pragma unroll
+        for (int s = 0; s < N; ++s) {
+          const V x = *reinterpret_cast<const V*>(stage + s * TB + q * 16);
+          memcpy(vals[s], &x, sizeof(x));
+        }
+        if constexpr (upd) {
+          const V x = *reinterpret_cast<const V*>(stage + N * TB + q * 16);
+          memcpy(w, &x, sizeof(x));
+        }
+        if constexpr (fast) {
+          const float4 x = *reinterpret_cast<const float4*>(stage + (N + 1) * TB + q * 16);
+          memcpy(vv, &x, sizeof(x));
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          T col[N];
+#pragma unroll
+          for (int s = 0; s < N; ++s) col[s] = vals[s][k];
+          T gsum;
+          if constexpr (sizeof(T) == 8)
+            gsum = tree_sum<N>(col, AddF64{});
+          else
+            gsum = tree_sum<N>(col, AddF32{});
+          w[k] = bulk_update<MODE, T>(upd ? w[k] : T(0), gsum, vv[k], lr, scale, mu, wd);
+        }
+        V xo;
+        memcpy(&xo, w, sizeof(xo));
+        *reinterpret_cast<V*>(stage + N * TB + q * 16) = xo;  // w slot holds the output (also when upd is off)
+        if constexpr (fast) {
+          float4 xv;
+          memcpy(&xv, vv, sizeof(xv));
+          *reinterpret_cast<float4*>(stage + (N + 1) * TB + q * 16) = xv;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma_store(wme + e0, stage + N * TB, nb);
+        for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + e0, stage + N * TB, nb);
+        if constexpr (fast) tma_store(a.v + e0, stage + (N + 1) * TB, nb);
+        tma_commit();
+        if (t + SO - 1 < nt) {
+          tma_wait_read<1>();  // stage (g - 1) % SO: its stores (the previous group) have read it
+          issue(t + SO - 1);
+        }
+      }
+    }
+    ouse += nt;
+    if (threadIdx.x == 0) tma_wait_read<0>();  // the LSU tail reuses the ring
+    __syncthreads();
+    return lo + body;
+  }
+}
+
 // wait until at most k bulk groups are still reading their shared-memory sources
 __device__ __forceinline__ void tma_wait_read_n(int k) {
   switch (k) {
@@ -688,12 +816,15 @@ __global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XAr
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + G::kRing);  // push ring mbarriers
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
+  __shared__ uint64_t obars[8];  // owner-tile mbarriers (owner_tma)
   if (threadIdx.x == 0) {
     for (int k = 0; k < S; ++k) mbar_init(&bars[k], 1);
+    for (int k = 0; k < 8; ++k) mbar_init(&obars[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   uint32_t gload = 0;  // thread 0's push load counter (mbarrier phases)
+  uint32_t ouse = 0;   // owner tiles consumed (owner_tma phases)
   const int me = a.rank;
   constexpr bool fast = MODE == PGX_MODE_FAST32;
   constexpr bool upd = MODE != PGX_MODE_SUM32;
@@ -763,13 +894,14 @@ __global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XAr
       const T* rx0 = static_cast<const T*>(a.rx[me]) + (uint64_t)parity * a.K * a.sl - (uint64_t)me * a.sl;
       T* wme = static_cast<T*>(a.model[me]);
       const T* gs = slab_grad<T>(a.g, lo, hi);
+      const uint64_t lo_lsu = owner_tma<N, T, MODE, LEAN>(a, rx0, gs, lo, hi, ring, obars, ouse);
       constexpr int U = N <= 4 ? 4 : 2;                         // vectors per thread per round
       const uint64_t RE = (uint64_t)blockDim.x * U * W;         // elements per round
       const int K = (int)(G::kRing / (RE * sizeof(T)));         // output ring slots
       unsigned long long t_ld = 0, t_ring = 0, t_st = 0, t_x = 0;
       const bool tr = a.trace && threadIdx.x == 0;
       uint32_t r = 0;
-      for (uint64_t t0 = lo; t0 < hi; t0 += RE, ++r) {
+      for (uint64_t t0 = lo_lsu; t0 < hi; t0 += RE, ++r) {  // the ragged (< 16 B) end, or an ineligible slab
         const uint64_t t1 = min(t0 + RE, hi);
         T* slot = reinterpret_cast<T*>(ring + (size_t)(r % K) * RE * sizeof(T));
         if (tr) t_x = globaltimer_ns();
