@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--gate", default="auto", choices=["auto", "layer", "model"],
                    help="per-layer forward gates, or one whole-model gate per step (auto: model if > 16 layers)")
     p.add_argument("--max-ctas", type=int, default=0)
-    p.add_argument("--large", choices=("ce", "cep", "sm", "bulk", "ceb"), default="ce",
+    p.add_argument("--large", choices=("ce", "cep", "sm", "bulk", "ceb", "cet"), default="ce",
                    help="auto policy for layers >= 1M elements: copy-engine or SM two-shot")
     p.add_argument("--large-ctas", type=int, default=0, help="CTA cap of the large layers' launches (0 = auto)")
     p.add_argument("--large-chunk-elems", type=int, default=0, help="chunk of the large layers (0 = --chunk-elems)")
@@ -731,6 +731,7 @@ def pgx_arm(args):
              "twoshot_cep": "k_twoshot owner items + copy-engine reduce-scatter",
              "twoshot_bulk": "k_twoshot_bulk (TMA bulk copies, capped grid)",
              "twoshot_ceb": "k_twoshot_bulk owner slabs (TMA all-gather) + copy-engine reduce-scatter",
+             "twoshot_cet": "k_owner_tma (TMA-fed fold + update, capped grid) + copy-engine reduce-scatter / all-gather",
              "tree": "k_tree_up/k_tree_down", "nvls": "k_nvls (multimem)",
              "oneshot": "k_oneshot", "twoshot_l128": "k_twoshot_l128 (128-byte lines, fence-free)",
              "oneshot_ll": "k_oneshot_ll", "oneshot_l128": "k_oneshot_l128"}[xchg.variants[L_DOM]]

@@ -228,9 +228,12 @@ enum pgx_xchg_flag {
   PGX_XF_ALLOW_L128 = 32,          /* permit ONESHOT_L128 / TWOSHOT_L128 layers (sm_100 only) */
   PGX_XF_BULK_LEAN = 64,           /* TWOSHOT_BULK: 256 threads + 64 KB ring per CTA (shares
                                       SMs with the backward) instead of 512 + 224 KB        */
-  PGX_XF_BULK_CE_RS = 128          /* TWOSHOT_BULK: reduce-scatter by the copy engines in
+  PGX_XF_BULK_CE_RS = 128,         /* TWOSHOT_BULK: reduce-scatter by the copy engines in
                                       part-major copies (per-part chunk signals); the kernel
                                       runs the owner slabs only (fold + update + TMA gather) */
+  PGX_XF_CE_TMA_OWNER = 256        /* TWOSHOT_CE: owner fold fed by TMA bulk loads on a capped
+                                      grid (layer_max_ctas, default 32) instead of the LSU
+                                      fold on every SM                                      */
 };
 
 typedef struct pgx_xchg_config {

@@ -34,6 +34,7 @@ VARIANT_TWOSHOT_L128 = 9
 XF_CE_RS_PARTS, XF_TMA, XF_ONESHOT_SMALL_CHUNKS, XF_AUTO_CHUNK_TREE, XF_NO_AUTO_CHUNK_NVLS, XF_ALLOW_L128 = 1, 2, 4, 8, 16, 32
 XF_BULK_LEAN = 64
 XF_BULK_CE_RS = 128
+XF_CE_TMA_OWNER = 256
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p

@@ -683,7 +683,8 @@ struct OwnerGeo {
 // Folds [lo, lo + body) of the owner slab (body: the 16-byte-granular prefix) through the
 // TMA pipeline; returns the first element NOT done (lo when the slab is not eligible).
 // `ouse` counts the tiles this CTA ever consumed (mbarrier phases), identical in all threads.
-template <int N, class T, int MODE, bool LEAN>
+// kGather = false (TWOSHOT_CE: the copy engines all-gather): local stores only.
+template <int N, class T, int MODE, bool LEAN, bool kGather = true>
 __device__ __forceinline__ uint64_t owner_tma(const XArgs& a, const T* rx0, const T* gs, uint64_t lo, uint64_t hi,
                                               uint8_t* ring, uint64_t* obars, uint32_t& ouse) {
   using OG = OwnerGeo<N, LEAN>;
@@ -702,7 +703,8 @@ __device__ __forceinline__ uint64_t owner_tma(const XArgs& a, const T* rx0, cons
     if (fast) al |= reinterpret_cast<uintptr_t>(a.v + lo);
     for (int s = 0; s < N; ++s)
       if (s != me) al |= reinterpret_cast<uintptr_t>(rx0 + (uint64_t)s * a.sl + lo);
-    for (int d = 1; d < N; ++d) al |= reinterpret_cast<uintptr_t>(static_cast<T*>(a.model[(me + d) % N]) + lo);
+    if constexpr (kGather)
+      for (int d = 1; d < N; ++d) al |= reinterpret_cast<uintptr_t>(static_cast<T*>(a.model[(me + d) % N]) + lo);
     if (al & 15) return lo;
     const uint64_t body = (((hi - lo) * sizeof(T)) & ~uint64_t(15)) / sizeof(T);
     const uint32_t nt = (uint32_t)((body + TE - 1) / TE);
@@ -775,7 +777,8 @@ __device__ __forceinline__ uint64_t owner_tma(const XArgs& a, const T* rx0, cons
       __syncthreads();
       if (threadIdx.x == 0) {
         tma_store(wme + e0, stage + N * TB, nb);
-        for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + e0, stage + N * TB, nb);
+        if constexpr (kGather)
+          for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + e0, stage + N * TB, nb);
         if constexpr (fast) tma_store(a.v + e0, stage + (N + 1) * TB, nb);
         tma_commit();
         if (t + SO - 1 < nt) {
@@ -1859,7 +1862,58 @@ __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
 }
 
 constexpr int kCepCtas = 48;  // TWOSHOT_CEP owner grid default
+constexpr int kCeTmaCtas = 32;  // TWOSHOT_CE + PGX_XF_CE_TMA_OWNER owner grid default
 constexpr uint64_t kAutoChunkMax = 65536;  // elements
+
+// TWOSHOT_CE owner fold on a capped grid (PGX_XF_CE_TMA_OWNER): the part [olo, ohi) split
+// into one contiguous 16-byte-aligned slab per CTA, each folded through owner_tma (TMA
+// loads of the N partials + w + v into the ring, fold + update from shared memory, bulk
+// stores of w / v).  On the full grid the fold of k_owner_local saturates HBM with every SM
+// waiting on it; a TMA-fed CTA moves ~1.5x more bytes per SM (ncu r6a), so a few dozen
+// CTAs do the same fold in far fewer SM-cycles while the copy engines move the shards.
+template <int N, class T, int MODE>
+__global__ void __launch_bounds__(BulkGeo<false>::kThreads, 1) k_owner_tma(XArgs a) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ uint64_t obars[8];
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 8; ++k) mbar_init(&obars[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int me = a.rank;
+  const uint64_t base = min((uint64_t)me * a.sl, a.S);
+  uint64_t lo = base, hi = min((uint64_t)(me + 1) * a.sl, a.S);
+  if (a.ohi) {
+    lo = a.olo;
+    hi = a.ohi;
+  }
+  if (lo >= hi) return;
+  const uint64_t per = ((hi - lo + gridDim.x - 1) / gridDim.x + 3) / 4 * 4;
+  const uint64_t slo = lo + (uint64_t)blockIdx.x * per, shi = min(hi, slo + per);
+  if (slo >= shi) return;
+  const T* rx0 = static_cast<const T*>(a.rx[me]) + (uint64_t)a.parity * a.K * a.sl - base;
+  const T* gs = slab_grad<T>(a.g, slo, shi);
+  uint32_t ouse = 0;
+  const uint64_t done = owner_tma<N, T, MODE, false, false>(a, rx0, gs, slo, shi, ring, obars, ouse);
+  if (threadIdx.x == 0) tma_wait_all();  // w / v stores complete before the kernel ends
+  // the ragged end (< 16 bytes) or an ineligible slab: element by element, same arithmetic
+  constexpr bool fast = MODE == PGX_MODE_FAST32;
+  constexpr bool upd = MODE != PGX_MODE_SUM32;
+  T* wme = static_cast<T*>(a.model[me]);
+  for (uint64_t e = done + threadIdx.x; e < shi; e += blockDim.x) {
+    T col[N];
+#pragma unroll
+    for (int s = 0; s < N; ++s) col[s] = (s == me) ? grad_elem<T>(a.g, e) : __ldcg(rx0 + (uint64_t)s * a.sl + e);
+    T gsum;
+    if constexpr (sizeof(T) == 8)
+      gsum = tree_sum<N>(col, AddF64{});
+    else
+      gsum = tree_sum<N>(col, AddF32{});
+    float vv = fast ? a.v[e] : 0.f;
+    wme[e] = bulk_update<MODE, T>(upd ? wme[e] : T(0), gsum, vv, a.lr, a.scale, a.mu, a.wd);
+    if (fast) a.v[e] = vv;
+  }
+}
 
 struct LayerPlan {
   uint64_t S = 0;
@@ -1937,6 +1991,7 @@ struct pgx_xchg {
   bool ce_rs_parts = false;                        // push signals per owner part (signals on ce_rs2)
   bool tma = false;  // TWOSHOT: push / all-gather as TMA bulk copies (PGX_TMA=1; slower fused at N=4, profiles/r1r)
   bool bulk_ce_rs = false;  // TWOSHOT_BULK: reduce-scatter by the copy engines (PGX_XF_BULK_CE_RS)
+  bool ce_tma_owner = false;  // TWOSHOT_CE: owner fold by k_owner_tma on a capped grid (PGX_XF_CE_TMA_OWNER)
   bool oneshot_small_chunks = false;  // PGX_ONESHOT_SMALL_CHUNKS=1: measured slower (profiles/r3v)
   bool auto_chunk_tree = false, auto_chunk_nvls = true;  // size-scaled chunks: NVLS yes, tree no (its pipeline
                                                         // fill grows with the chunk; profiles/r3r)
@@ -2167,6 +2222,36 @@ void launch_oneshot_ll(int N, int want, int dev, cudaStream_t s, const XArgs& a)
   case n:                                                                      \
     k_oneshot_ll<n><<<oneshot_ll_grid<n>(want, dev), kThreads, 0, s>>>(a);   \
     break;
+    PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
+#undef PGX_CASE
+  }
+}
+
+template <int N, class T, int MODE>
+void launch_owner_tma_nm(int grid, int dev, cudaStream_t s, const XArgs& a) {
+  using G = BulkGeo<false>;
+  static bool attr[64] = {};  // per device
+  if (!attr[dev & 63]) {
+    cudaFuncSetAttribute(k_owner_tma<N, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem);
+    attr[dev & 63] = true;
+  }
+  k_owner_tma<N, T, MODE><<<grid, G::kThreads, G::kSmem, s>>>(a);
+}
+
+template <int N>
+void launch_owner_tma_n(int mode, int grid, int dev, cudaStream_t s, const XArgs& a) {
+  switch (mode) {
+    case PGX_MODE_REF64: launch_owner_tma_nm<N, double, PGX_MODE_REF64>(grid, dev, s, a); break;
+    case PGX_MODE_REF32: launch_owner_tma_nm<N, float, PGX_MODE_REF32>(grid, dev, s, a); break;
+    case PGX_MODE_SUM32: launch_owner_tma_nm<N, float, PGX_MODE_SUM32>(grid, dev, s, a); break;
+    default: launch_owner_tma_nm<N, float, PGX_MODE_FAST32>(grid, dev, s, a); break;
+  }
+}
+
+void launch_owner_tma(int N, int mode, int grid, int dev, cudaStream_t s, const XArgs& a) {
+  switch (N) {
+#define PGX_CASE(n) \
+  case n: launch_owner_tma_n<n>(mode, grid, dev, s, a); break;
     PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
 #undef PGX_CASE
   }
@@ -2505,7 +2590,11 @@ static int launch_twoshot_ce(pgx_xchg* x, int l, const LayerPlan& P, XArgs& a, c
       a.olo = plo;
       a.ohi = phi;
       int grid = std::max(1, std::min(P.grid, (int)(((phi - plo) / VecT<float>::W + kThreads - 1) / kThreads)));
-      if (phi > plo) {
+      if (phi > plo && x->ce_tma_owner) {
+        launch_owner_tma(N, x->cfg.mode, std::max(1, std::min(P.grid, (int)((phi - plo + 8191) / 8192))), x->dev,
+                         x->ce_own, a);
+        ++x->launches;
+      } else if (phi > plo) {
         if (esz == 8)
           launch_owner_local<double>(N, grid, x->ce_own, a);
         else
@@ -2724,6 +2813,7 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
   x->oneshot_small_chunks = (cfg->flags & PGX_XF_ONESHOT_SMALL_CHUNKS) != 0;
   x->tma = (cfg->flags & PGX_XF_TMA) != 0;
   x->bulk_ce_rs = (cfg->flags & PGX_XF_BULK_CE_RS) != 0;
+  x->ce_tma_owner = (cfg->flags & PGX_XF_CE_TMA_OWNER) != 0;
   x->ce_rs_parts = (cfg->flags & PGX_XF_CE_RS_PARTS) != 0;
   if (cfg->ce_parts) x->ce_parts = cfg->ce_parts;
   if (cfg->ce_rs_streams) x->ce_rs_streams = cfg->ce_rs_streams;
@@ -2782,6 +2872,10 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     bool capped = lcapped || cfg->max_ctas > 0;
     if (P.variant == PGX_VARIANT_TWOSHOT_CEP && !capped) {  // 48 CTAs saturate NVLink (profiles/r3h)
       cap = std::min(cap, kCepCtas);
+      capped = true;
+    }
+    if (P.variant == PGX_VARIANT_TWOSHOT_CE && x->ce_tma_owner && !capped) {
+      cap = kCeTmaCtas;
       capped = true;
     }
     if (P.variant == PGX_VARIANT_TWOSHOT_BULK && !capped) {  // 16-24 TMA CTAs saturate NVLink (r3d)

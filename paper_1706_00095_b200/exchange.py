@@ -28,11 +28,15 @@ VARIANTS = {"tree": _lib.VARIANT_TREE, "twoshot": _lib.VARIANT_TWOSHOT, "twoshot
             "oneshot_ll": _lib.VARIANT_ONESHOT_LL, "oneshot_l128": _lib.VARIANT_ONESHOT_L128,
             "twoshot_bulk": _lib.VARIANT_TWOSHOT_BULK, "twoshot_l128": _lib.VARIANT_TWOSHOT_L128,
             # TWOSHOT_BULK with its reduce-scatter on the copy engines (the bulk_ce_rs flag)
-            "twoshot_ceb": _lib.VARIANT_TWOSHOT_BULK}
-VARIANT_ALIASES = {"twoshot_ceb": ("twoshot_bulk", "bulk_ce_rs")}  # Python name -> (library variant, flag)
+            "twoshot_ceb": _lib.VARIANT_TWOSHOT_BULK,
+            # TWOSHOT_CE with the owner fold fed by TMA loads on a capped grid (the ce_tma_owner flag)
+            "twoshot_cet": _lib.VARIANT_TWOSHOT_CE}
+VARIANT_ALIASES = {"twoshot_ceb": ("twoshot_bulk", "bulk_ce_rs"),  # Python name -> (library variant, flag)
+                   "twoshot_cet": ("twoshot_ce", "ce_tma_owner")}
 FLAGS = {"ce_rs_parts": _lib.XF_CE_RS_PARTS, "tma": _lib.XF_TMA, "oneshot_small_chunks": _lib.XF_ONESHOT_SMALL_CHUNKS,
          "auto_chunk_tree": _lib.XF_AUTO_CHUNK_TREE, "no_auto_chunk_nvls": _lib.XF_NO_AUTO_CHUNK_NVLS,
-         "allow_l128": _lib.XF_ALLOW_L128, "bulk_lean": _lib.XF_BULK_LEAN, "bulk_ce_rs": _lib.XF_BULK_CE_RS}
+         "allow_l128": _lib.XF_ALLOW_L128, "bulk_lean": _lib.XF_BULK_LEAN, "bulk_ce_rs": _lib.XF_BULK_CE_RS,
+         "ce_tma_owner": _lib.XF_CE_TMA_OWNER}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 
@@ -72,7 +76,7 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
         return "oneshot"
     if world > 1 and elems >= ce_from:
         return {"ce": "twoshot_ce", "cep": "twoshot_cep", "sm": "twoshot", "bulk": "twoshot_bulk",
-                "ceb": "twoshot_ceb"}[large]
+                "ceb": "twoshot_ceb", "cet": "twoshot_cet"}[large]
     return "twoshot"
 
 
@@ -117,6 +121,11 @@ class DeviceExchange:
                 raise ConfigError("twoshot_bulk and twoshot_ceb layers cannot be mixed in one exchange")
             if "bulk_ce_rs" not in flags:
                 flags += ("bulk_ce_rs",)
+        if "twoshot_cet" in variants:  # one library flag switches every copy-engine layer's owner fold
+            if "twoshot_ce" in variants:
+                raise ConfigError("twoshot_ce and twoshot_cet layers cannot be mixed in one exchange")
+            if "ce_tma_owner" not in flags:
+                flags += ("ce_tma_owner",)
         self.variants = variants
         self.scale = 1.0 / self.world if scale is None else float(scale)
         self._elems = (C.c_uint64 * L)(*self.layer_elems)

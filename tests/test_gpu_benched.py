@@ -45,22 +45,22 @@ def _bits_equal(t, a):
     return torch.equal(t.view(torch.int32), want.view(torch.int32))
 
 
-def _expected_variants(sizes, N, mode):
+def _expected_variants(sizes, N, mode, large="ce"):
     from paper_1706_00095_b200.exchange import L128_BAND, choose_variant
 
     ll = (1 << 16) if mode != "ref64" else 0
     band = L128_BAND if mode != "ref64" else (0, 0)
-    return [choose_variant(n, N, 0, ce_from=1 << 20, large="ce", ll_below=ll, l128_range=band) for n in sizes]
+    return [choose_variant(n, N, 0, ce_from=1 << 20, large=large, ll_below=ll, l128_range=band) for n in sizes]
 
 
-def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER):
+def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER, large="ce"):
     from paper_1706_00095_b200.exchange import L128_BAND
 
     hyper = fast_hyper if mode == "fast32" else dict(lr=0.05)
     # bench.py's defaults: --l128 = L128_BAND (with the allow_l128 opt-in), large layers "ce"
     world, trs, xs = build(N, sizes, mode, "auto", chunk_elems=16384, flags=("allow_l128",), l128_range=L128_BAND,
-                           **hyper)
-    assert xs[0].variants == _expected_variants(sizes, N, mode)
+                           large=large, **hyper)
+    assert xs[0].variants == _expected_variants(sizes, N, mode, large)
     w = [O.seeded_fill(42 ^ l, n, 1.0 / np.sqrt(n)).astype(np.float32) for l, n in enumerate(sizes)]
     v = [np.zeros(n, np.float32) for n in sizes]
     for x in xs:
@@ -98,10 +98,12 @@ def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER):
 
 @pytest.mark.parametrize("N", [2, 4, 8])
 @pytest.mark.parametrize("mode", ["fast32", "ref32"])
-def test_alexnet_auto_plan_matches_oracle(cuda, N, mode):
+@pytest.mark.parametrize("large", ["ce", "cet", "bulk"])
+def test_alexnet_auto_plan_matches_oracle(cuda, N, mode, large):
     """The AlexNet step's exchange plan (copy-engine two-shot with 3-4 owner parts for
-    fc6/fc7/fc8, auto-sized chunks elsewhere), two iterations, every rank bit-exact."""
-    _run(N, ALEXNET, mode, iters=2, gate="layer")
+    fc6/fc7/fc8, auto-sized chunks elsewhere), two iterations, every rank bit-exact; also
+    with bench.py's --large cet (TMA-fed owner fold) and --large bulk (TMA bulk kernel)."""
+    _run(N, ALEXNET, mode, iters=2, gate="layer", large=large)
 
 
 def test_alexnet_plan_has_multipart_owners(cuda):

@@ -38,7 +38,7 @@ def stepped_layer(xs, trs, l, k, pieces_by_rank, gate=True):
     N = len(xs)
     sync = torch.cuda.synchronize
     if xs[0].variants[l] in ("twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128",
-                            "twoshot_bulk", "twoshot_ceb"):
+                            "twoshot_bulk", "twoshot_ceb", "twoshot_cet"):
         for r in range(N):
             xs[r].launch(l, k, pieces_by_rank[r], stream=trs[r].stream, phases=_lib.PHASE_PUSH)
         sync()
@@ -73,7 +73,7 @@ def split_pieces(g, cut):
 
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128", "twoshot_ceb"])
+                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128", "twoshot_ceb", "twoshot_cet"])
 @pytest.mark.parametrize("mode", ["ref32", "fast32", "ref64", "sum32"])
 def test_exchange_matches_oracle(cuda, N, variant, mode):
     if variant in ("oneshot_ll", "oneshot_l128", "twoshot_l128") and mode == "ref64":
@@ -186,7 +186,7 @@ class _FixedGrad(torch.nn.Module):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "twoshot_bulk",
-                                     "twoshot_l128", "twoshot_ceb"])
+                                     "twoshot_l128", "twoshot_ceb", "twoshot_cet"])
 @pytest.mark.parametrize("gate", ["layer", "model"])
 def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
     """A captured training step (device iteration counter) applies exactly the oracle update."""
@@ -236,7 +236,7 @@ def test_cuda_graph_replay_matches_oracle(cuda, variant, gate):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll",
-                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128", "twoshot_ceb"])
+                                     "oneshot_l128", "twoshot_bulk", "twoshot_l128", "twoshot_ceb", "twoshot_cet"])
 def test_tiny_and_ragged_layers_at_eight_ranks(cuda, variant):
     """Layers smaller than one vector per rank (empty owner shards), ragged tails and a
     piece boundary inside a vector, 8 ranks stepped on one GPU, ref32 bit-exact."""
@@ -382,7 +382,7 @@ def test_ceb_part_major_reduce_scatter_matches_oracle(cuda, N):
 
 
 @pytest.mark.parametrize("variant", ["twoshot", "tree", "twoshot_ce", "oneshot", "oneshot_ll", "twoshot_bulk",
-                                     "twoshot_l128", "twoshot_ceb"])
+                                     "twoshot_l128", "twoshot_ceb", "twoshot_cet"])
 def test_misaligned_gradient_views_match_oracle(cuda, variant):
     """Gradient pieces that are views at 4- and 12-byte offsets into larger buffers (not
     16-byte aligned): the kernels must fall back from the per-slab vector path to the

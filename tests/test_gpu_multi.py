@@ -109,7 +109,7 @@ def _ngpu():
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("variant,mode", [(v, m) for v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "oneshot", "oneshot_ll", "oneshot_l128",
-                                                                    "twoshot_bulk", "twoshot_l128", "twoshot_ceb")
+                                                                    "twoshot_bulk", "twoshot_l128", "twoshot_ceb", "twoshot_cet")
                                           for m in ("ref32", "fast32")]
                          + [("nvls", "fast32")])
 def test_concurrent_exchange_matches_oracle(variant, mode):
@@ -399,7 +399,7 @@ def _graph_worker(rank, world, port, variant, gate, use_graph, q):
                                           ("twoshot_ce", "layer"), ("twoshot_cep", "model"), ("tree", "layer"),
                                           ("oneshot", "layer"), ("oneshot_ll", "model"), ("oneshot_l128", "layer"),
                                           ("twoshot_bulk", "layer"), ("twoshot_bulk", "model"),
-                                          ("twoshot_l128", "model"), ("twoshot_ceb", "layer")])
+                                          ("twoshot_l128", "model"), ("twoshot_ceb", "layer"), ("twoshot_cet", "layer")])
 def test_graph_replay_multi_gpu_matches_oracle(variant, gate):
     out = _spawn(_graph_worker, _ngpu(), variant, gate, True)
     for rank, bad, status in out:

@@ -65,7 +65,7 @@ def main():
     seg = 16
     for v in variants:
         if v in ("twoshot", "tree", "twoshot_ce", "twoshot_cep", "nvls", "oneshot", "oneshot_ll", "oneshot_l128",
-                 "twoshot_bulk", "twoshot_l128"):
+                 "twoshot_bulk", "twoshot_l128", "twoshot_ceb", "twoshot_cet"):
             xs[v] = DeviceExchange(tr, elems, mode=args.mode, variant=v, chunk_elems=args.chunk, lr=0.01,
                                    momentum=0.9, weight_decay=5e-4, seg_base=seg, max_ctas=args.ctas,
                                    flags=tuple(f for f in args.xflags.split(",") if f)
