@@ -665,13 +665,17 @@ __device__ __forceinline__ T bulk_update(T w, T g, float& v, double lr, float sc
 
 // Owner fold fed by TMA loads.  The LSU path (one 16-byte load per thread and stream)
 // keeps ~48 KB in flight per SM and was lg_throttle-bound at ~39 GB/s per SM (ncu r5z:
-// the 24-CTA owner phase of fc6 ran 395 us); bulk loads keep SO-1 whole tiles of all
-// N + 2 input streams (N partials, w, v) in flight per CTA with no LSU slots at all.
-// Per tile: one elected thread issues the N + 2 cp.async.bulk loads onto the stage's
-// mbarrier; every thread folds its vectors from shared memory in tree order, applies
-// the fused update and writes w / v back IN PLACE; the elected thread then bulk-stores
-// the w tile into the local and every peer's weights and the v tile into the local
-// momentum.  A stage is reloaded only after wait_group.read says its stores have read it.
+// the 24-CTA owner phase of fc6 ran 395 us); bulk loads keep whole tiles of all N + 2
+// input streams (N partials, w, v) in flight per CTA with no LSU slots at all.
+// Warp-specialised: thread 0 of warp 0 is the producer — it issues the N + 2
+// cp.async.bulk loads of a tile onto the stage's `full` mbarrier, waits on the stage's
+// `done` mbarrier, bulk-stores the updated w tile into the local and every peer's
+// weights and the v tile into the local momentum, and reloads a stage once
+// wait_group.read says its stores have read it.  Warps 1.. are the consumers: wait
+// `full`, fold their vectors from shared memory in tree order, apply the fused update,
+// write w / v back IN PLACE and arrive on `done` (one arrival per warp).  No CTA-wide
+// barrier per tile, so the consumers never wait for the producer's store bookkeeping
+// (the first cut's per-tile __syncthreads left 0.55 eligible warps per scheduler, r6c).
 template <int N, bool LEAN>
 struct OwnerGeo {
   static constexpr int kTile = LEAN ? (N <= 4 ? 4096 : 2048) : (N <= 4 ? 8192 : 4096);  // bytes per stream
@@ -680,9 +684,14 @@ struct OwnerGeo {
   static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // Folds [lo, lo + body) of the owner slab (body: the 16-byte-granular prefix) through the
 // TMA pipeline; returns the first element NOT done (lo when the slab is not eligible).
 // `ouse` counts the tiles this CTA ever consumed (mbarrier phases), identical in all threads.
+// obars[0..7] = full, obars[8..15] = done (count: consumer warps).
 // kGather = false (TWOSHOT_CE: the copy engines all-gather): local stores only.
 template <int N, class T, int MODE, bool LEAN, bool kGather = true>
 __device__ __forceinline__ uint64_t owner_tma(const XArgs& a, const T* rx0, const T* gs, uint64_t lo, uint64_t hi,
@@ -709,86 +718,98 @@ __device__ __forceinline__ uint64_t owner_tma(const XArgs& a, const T* rx0, cons
     const uint64_t body = (((hi - lo) * sizeof(T)) & ~uint64_t(15)) / sizeof(T);
     const uint32_t nt = (uint32_t)((body + TE - 1) / TE);
     if (nt == 0) return lo;
-    constexpr uint32_t nstream = N + (upd ? 1 : 0) + (fast ? 1 : 0);
-    auto issue = [&](uint32_t i) {  // tile i of the slab -> stage (ouse + i) % SO
-      const uint64_t e0 = lo + (uint64_t)i * TE;
-      const uint32_t nb = (uint32_t)(min((uint64_t)TE, lo + body - e0) * sizeof(T));
-      const uint32_t st = (ouse + i) % SO;
-      uint8_t* stage = ring + (size_t)st * OG::kStage;
-      mbar_expect_tx(&obars[st], nb * nstream);
-#pragma unroll
-      for (int s = 0; s < N; ++s)
-        tma_load(stage + s * TB, (s == me) ? gs + (e0 - lo) : rx0 + (uint64_t)s * a.sl + e0, nb, &obars[st]);
-      if constexpr (upd) tma_load(stage + N * TB, wme + e0, nb, &obars[st]);
-      if constexpr (fast) tma_load(stage + (N + 1) * TB, a.v + e0, nb, &obars[st]);
-    };
+    uint64_t* full = obars;
+    uint64_t* done = obars + 8;
+    auto tile_bytes = [&](uint32_t t) { return (uint32_t)(min((uint64_t)TE, lo + body - (lo + (uint64_t)t * TE)) * sizeof(T)); };
     if (threadIdx.x == 0) {
+      // ---- producer
+      constexpr uint32_t nstream = N + (upd ? 1 : 0) + (fast ? 1 : 0);
+      auto issue = [&](uint32_t i) {  // tile i of the slab -> stage (ouse + i) % SO
+        const uint64_t e0 = lo + (uint64_t)i * TE;
+        const uint32_t nb = tile_bytes(i);
+        const uint32_t st = (ouse + i) % SO;
+        uint8_t* stage = ring + (size_t)st * OG::kStage;
+        mbar_expect_tx(&full[st], nb * nstream);
+#pragma unroll
+        for (int s = 0; s < N; ++s)
+          tma_load(stage + s * TB, (s == me) ? gs + (e0 - lo) : rx0 + (uint64_t)s * a.sl + e0, nb, &full[st]);
+        if constexpr (upd) tma_load(stage + N * TB, wme + e0, nb, &full[st]);
+        if constexpr (fast) tma_load(stage + (N + 1) * TB, a.v + e0, nb, &full[st]);
+      };
       asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired rx data -> async-proxy reads
-      for (uint32_t i = 0; i < min(nt, (uint32_t)SO - 1); ++i) issue(i);
-    }
-    using V = typename VecT<T>::V;
-    constexpr int W = VecT<T>::W;
-    const double lr = a.lr;
-    const float scale = a.scale, mu = a.mu, wd = a.wd;
-    for (uint32_t t = 0; t < nt; ++t) {
-      const uint32_t g = ouse + t, st = g % SO;
-      const uint64_t e0 = lo + (uint64_t)t * TE;
-      const uint32_t nb = (uint32_t)(min((uint64_t)TE, lo + body - e0) * sizeof(T));
-      uint8_t* stage = ring + (size_t)st * OG::kStage;
-      mbar_wait(&obars[st], (g / SO) & 1u);
-      for (uint32_t q = threadIdx.x; q < nb / 16; q += blockDim.x) {
-        T vals[N][W], w[W];
-        float vv[W];
-#pragma unroll
-        for (int s = 0; s < N; ++s) {
-          const V x = *reinterpret_cast<const V*>(stage + s * TB + q * 16);
-          memcpy(vals[s], &x, sizeof(x));
-        }
-        if constexpr (upd) {
-          const V x = *reinterpret_cast<const V*>(stage + N * TB + q * 16);
-          memcpy(w, &x, sizeof(x));
-        }
-        if constexpr (fast) {
-          const float4 x = *reinterpret_cast<const float4*>(stage + (N + 1) * TB + q * 16);
-          memcpy(vv, &x, sizeof(x));
-        }
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-          T col[N];
-#pragma unroll
-          for (int s = 0; s < N; ++s) col[s] = vals[s][k];
-          T gsum;
-          if constexpr (sizeof(T) == 8)
-            gsum = tree_sum<N>(col, AddF64{});
-          else
-            gsum = tree_sum<N>(col, AddF32{});
-          w[k] = bulk_update<MODE, T>(upd ? w[k] : T(0), gsum, vv[k], lr, scale, mu, wd);
-        }
-        V xo;
-        memcpy(&xo, w, sizeof(xo));
-        *reinterpret_cast<V*>(stage + N * TB + q * 16) = xo;  // w slot holds the output (also when upd is off)
-        if constexpr (fast) {
-          float4 xv;
-          memcpy(&xv, vv, sizeof(xv));
-          *reinterpret_cast<float4*>(stage + (N + 1) * TB + q * 16) = xv;
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
-      __syncthreads();
-      if (threadIdx.x == 0) {
+      for (uint32_t i = 0; i < min(nt, (uint32_t)SO); ++i) issue(i);
+      for (uint32_t t = 0; t < nt; ++t) {
+        const uint32_t g = ouse + t, st = g % SO;
+        const uint64_t e0 = lo + (uint64_t)t * TE;
+        const uint32_t nb = tile_bytes(t);
+        uint8_t* stage = ring + (size_t)st * OG::kStage;
+        mbar_wait(&done[st], (g / SO) & 1u);  // the consumers wrote the tile's w / v
         tma_store(wme + e0, stage + N * TB, nb);
         if constexpr (kGather)
           for (int d = 1; d < N; ++d) tma_store(static_cast<T*>(a.model[(me + d) % N]) + e0, stage + N * TB, nb);
         if constexpr (fast) tma_store(a.v + e0, stage + (N + 1) * TB, nb);
         tma_commit();
-        if (t + SO - 1 < nt) {
-          tma_wait_read<1>();  // stage (g - 1) % SO: its stores (the previous group) have read it
-          issue(t + SO - 1);
+        if (t >= 1 && t - 1 + SO < nt) {
+          tma_wait_read<1>();  // the stores of tile t - 1 have read its stage
+          issue(t - 1 + SO);
         }
+      }
+      tma_wait_read<0>();  // the ring is free for the next slab / the LSU tail
+    } else if (threadIdx.x >= 32) {
+      // ---- consumers
+      using V = typename VecT<T>::V;
+      constexpr int W = VecT<T>::W;
+      const double lr = a.lr;
+      const float scale = a.scale, mu = a.mu, wd = a.wd;
+      const uint32_t ct = threadIdx.x - 32, nct = blockDim.x - 32;
+      for (uint32_t t = 0; t < nt; ++t) {
+        const uint32_t g = ouse + t, st = g % SO;
+        const uint32_t nb = tile_bytes(t);
+        uint8_t* stage = ring + (size_t)st * OG::kStage;
+        mbar_wait(&full[st], (g / SO) & 1u);
+        for (uint32_t q = ct; q < nb / 16; q += nct) {
+          T vals[N][W], w[W];
+          float vv[W];
+#pragma unroll
+          for (int s = 0; s < N; ++s) {
+            const V x = *reinterpret_cast<const V*>(stage + s * TB + q * 16);
+            memcpy(vals[s], &x, sizeof(x));
+          }
+          if constexpr (upd) {
+            const V x = *reinterpret_cast<const V*>(stage + N * TB + q * 16);
+            memcpy(w, &x, sizeof(x));
+          }
+          if constexpr (fast) {
+            const float4 x = *reinterpret_cast<const float4*>(stage + (N + 1) * TB + q * 16);
+            memcpy(vv, &x, sizeof(x));
+          }
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            T col[N];
+#pragma unroll
+            for (int s = 0; s < N; ++s) col[s] = vals[s][k];
+            T gsum;
+            if constexpr (sizeof(T) == 8)
+              gsum = tree_sum<N>(col, AddF64{});
+            else
+              gsum = tree_sum<N>(col, AddF32{});
+            w[k] = bulk_update<MODE, T>(upd ? w[k] : T(0), gsum, vv[k], lr, scale, mu, wd);
+          }
+          V xo;
+          memcpy(&xo, w, sizeof(xo));
+          *reinterpret_cast<V*>(stage + N * TB + q * 16) = xo;  // w slot holds the output (also when upd is off)
+          if constexpr (fast) {
+            float4 xv;
+            memcpy(&xv, vv, sizeof(xv));
+            *reinterpret_cast<float4*>(stage + (N + 1) * TB + q * 16) = xv;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> async proxy
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&done[st]);
       }
     }
     ouse += nt;
-    if (threadIdx.x == 0) tma_wait_read<0>();  // the LSU tail reuses the ring
     __syncthreads();
     return lo + body;
   }
@@ -819,10 +840,11 @@ __global__ void __launch_bounds__(BulkGeo<LEAN>::kThreads, 1) k_twoshot_bulk(XAr
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + G::kRing);  // push ring mbarriers
   __shared__ uint32_t s_item;
   __shared__ uint32_t* s_flags[PGX_MAX_RANKS];
-  __shared__ uint64_t obars[8];  // owner-tile mbarriers (owner_tma)
+  __shared__ uint64_t obars[16];  // owner-tile mbarriers (owner_tma): full[8], done[8]
   if (threadIdx.x == 0) {
     for (int k = 0; k < S; ++k) mbar_init(&bars[k], 1);
     for (int k = 0; k < 8; ++k) mbar_init(&obars[k], 1);
+    for (int k = 8; k < 16; ++k) mbar_init(&obars[k], blockDim.x / 32 - 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -1874,9 +1896,10 @@ constexpr uint64_t kAutoChunkMax = 65536;  // elements
 template <int N, class T, int MODE>
 __global__ void __launch_bounds__(BulkGeo<false>::kThreads, 1) k_owner_tma(XArgs a) {
   extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ uint64_t obars[8];
+  __shared__ uint64_t obars[16];
   if (threadIdx.x == 0) {
     for (int k = 0; k < 8; ++k) mbar_init(&obars[k], 1);
+    for (int k = 8; k < 16; ++k) mbar_init(&obars[k], blockDim.x / 32 - 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
