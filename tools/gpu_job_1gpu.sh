@@ -1,24 +1,15 @@
 #!/bin/bash
-# 1-GPU job: the driver's GPU suite, then ncu captures of the exchange kernels stepped on one
-# GPU (N=4 emulated; each command first exits 0 without ncu).  r5q.
+# r6f (1 GPU): driver rehearsal on the round-2 build (full -m gpu suite, smoke, N=1 bench +
+# reference arm), N=1 fused-update chunk/CTA sweep (tools/prof_update.py), compute-only
+# AlexNet fwd+bwd at B=256/64/32 (tools/fwdbwd_variants.py).
 cd "$(dirname "$0")/.." || exit 1
 O=gpurun_out
+R=${R:-r6f}
 mkdir -p $O
-# (suite ran in r5q)
-
-
-
-FC6=37752832
-run() {  # name variants regex skip count [elems]
-  local name=$1 var=$2 rx=$3 sk=$4 cnt=$5 el=${6:-$FC6}
-  local cmd="python tools/ncu_stepped.py --world 4 --elems $el --variants $var --iters 2"
-  timeout 300 $cmd > $O/r5q_plain_$name.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$rx" -s $sk -c $cnt \
-      -o $O/r5q_ncu_$name $cmd > $O/r5q_ncu_$name.log 2>&1
-  echo "ncu $name rc=$?"
-}
-run twoshot4 twoshot "k_twoshot<.int.4," 8 5
-run bulk4 twoshot_bulk "k_twoshot_bulk<.int.4," 8 5
-run ce4 twoshot_ce "k_owner_local<.int.4," 16 4
-run ll4 oneshot_ll "k_oneshot_ll<.int.4>" 8 5 65536
-run oneshot4 oneshot "k_oneshot<.int.4," 8 5 262144
+timeout 600 python tools/prof_update.py 16384:0 4096:0 8192:0 32768:0 65536:0 16384:296 8192:296 4096:296 2048:0 > $O/${R}_prof_update.jsonl 2> $O/${R}_prof_update.err; echo "prof rc=$?"
+timeout 1500 python -m pytest tests -m gpu -x -q > $O/${R}_pytest_gpu_1gpu.log 2>&1; echo "suite rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/${R}_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python bench.py > $O/${R}_bench1.json 2> $O/${R}_bench1.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference > $O/${R}_bench1_ref.json 2> $O/${R}_bench1_ref.err; echo "ref rc=$?"
+timeout 600 python tools/fwdbwd_variants.py > $O/${R}_fwdbwd.log 2>&1; echo "fwdbwd rc=$?"
+echo done
