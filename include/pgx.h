@@ -243,7 +243,9 @@ typedef struct pgx_xchg_config {
   int mode;                      /* pgx_mode (REF64 uses double elements) */
   uint64_t chunk_elems;          /* notification granularity, multiple of 4; with N > 1
                                     the two-shot variants double it up to 65536 while a
-                                    shard still has >= 128 chunks (fewer system fences) */
+                                    shard still has >= 128 chunks (fewer system fences);
+                                    with N = 1 the two-shot (the fused update alone) caps
+                                    it at 4096 (shorter last wave)                      */
   double lr;                     /* epsilon / learning rate */
   float scale, momentum, weight_decay;
   uint32_t seg_base;             /* segment ids seg_base (weights + arrival flags) and

@@ -1886,6 +1886,7 @@ __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
 constexpr int kCepCtas = 48;  // TWOSHOT_CEP owner grid default
 constexpr int kCeTmaCtas = 32;  // TWOSHOT_CE + PGX_XF_CE_TMA_OWNER owner grid default
 constexpr uint64_t kAutoChunkMax = 65536;  // elements
+constexpr uint64_t kN1Chunk = 4096;        // elements per item of a one-rank (update-only) launch
 
 // TWOSHOT_CE owner fold on a capped grid (PGX_XF_CE_TMA_OWNER): the part [olo, ohi) split
 // into one contiguous 16-byte-aligned slab per CTA, each folded through owner_tma (TMA
@@ -2874,6 +2875,12 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
       // N=4: 40 vs 46 us, profiles/r3x)
       if (P.variant == PGX_VARIANT_TWOSHOT && shard <= (1u << 18) && c >= 8192 && c == CH) c /= 2;
       CH = c;
+    }
+    if (!ch_given && N == 1 && P.variant == PGX_VARIANT_TWOSHOT && CH > kN1Chunk) {
+      // one rank: the launch is the fused update alone, a pure HBM stream; 4 K-element items
+      // keep the last wave short (fc6 alone: 0.938 of the HBM peak with 16 K, 0.987 with 4 K;
+      // 2 K items pay more in claims than they save, profiles/r6f_prof_update.jsonl)
+      CH = kN1Chunk;
     }
     if (CH < 4 || CH % 4) {
       delete x;
