@@ -33,6 +33,14 @@ def build(lrn, conv1_nchw):
     return m
 
 
+# env: OPT=sgd|none (plain SGD step inside the graph or fwd+bwd alone), BATCHES=256,64,32,
+# FAST=1 (only bench.py's formulation: torch LRN, channels-last conv1)
+OPT = os.environ.get("OPT", "sgd")
+BATCHES = [int(b) for b in os.environ.get("BATCHES", "256,64,32").split(",")]
+LRNS = ("torch",) if os.environ.get("FAST") else ("torch", "window")
+C1S = (False,) if os.environ.get("FAST") else (False, True)
+
+
 def run(lrn, conv1_nchw, B, steps=20):
     torch.manual_seed(0)
     m = build(lrn, conv1_nchw)
@@ -56,7 +64,8 @@ def run(lrn, conv1_nchw, B, steps=20):
                 out = m(xin)
         loss = F.cross_entropy(out.float(), y)
         loss.backward()
-        opt.step()
+        if OPT == "sgd":
+            opt.step()
         opt.zero_grad(set_to_none=False)
         return loss
     torch.backends.cudnn.benchmark = True
@@ -84,7 +93,7 @@ t = torch.randn(4, 96, 27, 27, device="cuda").contiguous(memory_format=torch.cha
 ref = nn.LocalResponseNorm(5, alpha=1e-4, beta=0.75)(t)
 got = LRNWindow()(t)
 print(json.dumps({"lrn_max_rel_err": float(((got - ref).abs() / ref.abs().clamp_min(1e-6)).max())}))
-for B in (256, 64, 32):
-    for lrn in ("torch", "window"):
-        for c1 in (False, True):
-            print(json.dumps({"B": B, "lrn": lrn, "conv1_nchw": c1, "ms": run(lrn, c1, B)}), flush=True)
+for B in BATCHES:
+    for lrn in LRNS:
+        for c1 in C1S:
+            print(json.dumps({"B": B, "lrn": lrn, "conv1_nchw": c1, "opt": OPT, "ms": run(lrn, c1, B)}), flush=True)
