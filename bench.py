@@ -64,6 +64,8 @@ def parse():
     p.add_argument("--low-priority-from", type=int, default=0,
                    help="layers with at least this many elements launch on a normal-priority stream (0 = off)")
     p.add_argument("--xflags", default="", help="comma-separated exchange flags (exchange.FLAGS), e.g. bulk_lean")
+    p.add_argument("--overlap-ctas", type=int, default=0,
+                   help="CTA cap of the small layers whose exchange overlaps the backward (all but layer 0); 0 = off")
     p.add_argument("--l128", default="%d:%d" % L128_BAND,
                    help="LO:HI elements sent by the 128-byte-line two-shot (adds allow_l128); '' = off")
     p.add_argument("--no-e2e", action="store_true")
@@ -284,7 +286,8 @@ def workload_config(world, args):
             "chunk_elems": args.chunk_elems, "large_layers": {"variant": args.large, "ctas": args.large_ctas,
                                                                "chunk_elems": args.large_chunk_elems},
             "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager",
-            "exchange_flags": args.xflags or None, "l128_range": args.l128 or None}
+            "exchange_flags": args.xflags or None, "l128_range": args.l128 or None,
+            "overlap_ctas": args.overlap_ctas or None}
 
 
 # ------------------------------------------------------------------ model
@@ -422,7 +425,8 @@ def pgx_arm(args):
                           scale=1.0 / world, max_ctas=args.max_ctas,
                           low_priority_from=args.low_priority_from or None, large=args.large,
                           large_ctas=args.large_ctas, large_chunk_elems=args.large_chunk_elems,
-                          flags=xflags_of(args), l128_range=l128_of(args), **wl["hyper"])
+                          flags=xflags_of(args), l128_range=l128_of(args), overlap_ctas=args.overlap_ctas,
+                          **wl["hyper"])
     gate = args.gate if args.gate != "auto" else ("model" if len(sizes) > 16 else "layer")
     bind = ModuleBinding(xchg, model.layers(), gate=gate)
     if world > 1:  # identical initial weights everywhere: broadcast rank 0's (plumbing, untimed)
