@@ -87,7 +87,7 @@ class DeviceExchange:
                  tree_below: int = 0, low_priority_from: int | None = None, large: str = "ce",
                  large_from: int = 1 << 20, large_ctas: int = 0, large_chunk_elems: int = 0,
                  layer_chunk_elems=None, layer_max_ctas=None, ce_parts: int = 0, ce_rs_streams: int = 0,
-                 flags=(), l128_range: tuple[int, int] = (0, 0), overlap_ctas: int = 0):
+                 flags=(), l128_range: tuple[int, int] = (0, 0), overlap_ctas: int = 16):
         """variant: one name, a per-layer list, or "auto" (choose_variant; `large` = "ce" or
         "sm" for layers of >= `large_from` elements).  Layers of >= `large_from` elements get
         `large_chunk_elems` / `large_ctas` (0 = the global chunk_elems / max_ctas): fewer CTAs
@@ -99,7 +99,8 @@ class DeviceExchange:
         the small layers (< `large_from`) whose exchange overlaps the rest of the backward —
         every layer but layer 0, the last one backward emits, whose exchange nothing hides and
         which keeps the full grid.  Fewer CTAs per hidden exchange leave the SMs to the
-        backward kernels (GoogLeNet N=4: 16 CTAs 9.64 ms/step vs 9.80 uncapped, r6j)."""
+        backward kernels (GoogLeNet N=4: 16 CTAs 9.67 ms/step vs 9.82-9.87 uncapped, AlexNet
+        N=4: 5.00-5.02 vs 5.05-5.07 ms, r6j/r6k); 0 = every layer on the full grid."""
         if mode not in MODES:
             raise ConfigError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
         flags = tuple(flags)

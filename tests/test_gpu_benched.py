@@ -53,11 +53,12 @@ def _expected_variants(sizes, N, mode, large="ce"):
     return [choose_variant(n, N, 0, ce_from=1 << 20, large=large, ll_below=ll, l128_range=band) for n in sizes]
 
 
-def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER, large="ce", overlap_ctas=0):
+def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER, large="ce", overlap_ctas=16):
     from paper_1706_00095_b200.exchange import L128_BAND
 
     hyper = fast_hyper if mode == "fast32" else dict(lr=0.05)
-    # bench.py's defaults: --l128 = L128_BAND (with the allow_l128 opt-in), large layers "ce"
+    # bench.py's defaults: --l128 = L128_BAND (with the allow_l128 opt-in), large layers "ce",
+    # --overlap-ctas 16
     world, trs, xs = build(N, sizes, mode, "auto", chunk_elems=16384, flags=("allow_l128",), l128_range=L128_BAND,
                            large=large, overlap_ctas=overlap_ctas, **hyper)
     if overlap_ctas:  # every small layer but layer 0 runs on the capped grid
