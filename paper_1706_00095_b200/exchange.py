@@ -87,7 +87,8 @@ class DeviceExchange:
                  tree_below: int = 0, low_priority_from: int | None = None, large: str = "ce",
                  large_from: int = 1 << 20, large_ctas: int = 0, large_chunk_elems: int = 0,
                  layer_chunk_elems=None, layer_max_ctas=None, ce_parts: int = 0, ce_rs_streams: int = 0,
-                 flags=(), l128_range: tuple[int, int] = (0, 0), overlap_ctas: int = 16):
+                 flags=(), l128_range: tuple[int, int] = (0, 0), overlap_ctas: int = 16,
+                 overlap_exposed: int = 1):
         """variant: one name, a per-layer list, or "auto" (choose_variant; `large` = "ce" or
         "sm" for layers of >= `large_from` elements).  Layers of >= `large_from` elements get
         `large_chunk_elems` / `large_ctas` (0 = the global chunk_elems / max_ctas): fewer CTAs
@@ -100,7 +101,9 @@ class DeviceExchange:
         every layer but layer 0, the last one backward emits, whose exchange nothing hides and
         which keeps the full grid.  Fewer CTAs per hidden exchange leave the SMs to the
         backward kernels (GoogLeNet N=4: 16 CTAs 9.67 ms/step vs 9.82-9.87 uncapped, AlexNet
-        N=4: 5.00-5.02 vs 5.05-5.07 ms, r6j/r6k); 0 = every layer on the full grid."""
+        N=4: 5.00-5.02 vs 5.05-5.07 ms, r6j/r6k); 0 = every layer on the full grid.
+        `overlap_exposed`: how many of the first layers (the last ones backward emits) keep
+        the full grid."""
         if mode not in MODES:
             raise ConfigError(f"mode must be one of {sorted(MODES)}, got {mode!r}")
         flags = tuple(flags)
@@ -141,7 +144,7 @@ class DeviceExchange:
             [int(large_chunk_elems) if b else 0 for b in big]
         ctas = list(layer_max_ctas) if layer_max_ctas is not None else [int(large_ctas) if b else 0 for b in big]
         if layer_max_ctas is None and auto and overlap_ctas > 0 and self.world > 1 and not max_ctas:
-            ctas = [c if (b or l == 0) else int(overlap_ctas) for l, (c, b) in enumerate(zip(ctas, big))]
+            ctas = [c if (b or l < max(1, overlap_exposed)) else int(overlap_ctas) for l, (c, b) in enumerate(zip(ctas, big))]
         if len(chunks) != L or len(ctas) != L:
             raise ConfigError("layer_chunk_elems / layer_max_ctas need one entry per layer")
         self._chunks_req = [int(c) for c in chunks]
