@@ -2,7 +2,7 @@
 # r6b (4 GPUs; r6a had a port typo): TMA-fed owner fold in TWOSHOT_BULK (owner_tma): bulk parity (1 and 4 GPUs),
 # ncu of the stepped bulk kernel (owner phase vs r5z's 395 us), N=4 sweeps at 24/48 CTAs,
 # in-step AlexNet N=4: ce default vs bulk 24 / 48 (/ lean 48).
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6b
 mkdir -p $O

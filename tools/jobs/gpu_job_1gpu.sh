@@ -2,7 +2,7 @@
 # r6g (1 GPU): one-rank fused update with 4 K-element items (kN1Chunk): N=1 sweep, full -m gpu
 # suite + smoke, N=1 bench x2, the bench's launch list (ncu gpu__time_duration) and an
 # ncu --set full capture of the fc6 update (traffic for roofline.traffic).
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=${R:-r6g}
 mkdir -p $O

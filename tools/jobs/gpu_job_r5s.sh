@@ -2,7 +2,7 @@
 # r5s (4 GPUs): TWOSHOT_L128 first light — stepped parity on one GPU, concurrent parity on
 # 2/4 GPUs, 1-16 MB sweeps at N=2/4 against the existing variants and NCCL; ref64 sweep row;
 # in-step AlexNet N=4 with lean bulk CTA caps.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 mkdir -p $O
 CUDA_VISIBLE_DEVICES=0 timeout 900 python -m pytest tests/test_gpu_exchange.py -m gpu -q -rA -k "l128" -x > $O/r5s_pytest_l128_1gpu.log 2>&1

@@ -2,7 +2,7 @@
 # r6c (4 GPUs): TWOSHOT_CE with the TMA-fed owner fold on a capped grid (twoshot_cet /
 # --large cet): parity (1 GPU stepped + 4 GPUs concurrent + graphs), ncu of the stepped
 # k_owner_tma vs k_owner_local, N=4 sweep, in-step AlexNet N=4 and N=2: ce vs cet caps.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6c
 mkdir -p $O

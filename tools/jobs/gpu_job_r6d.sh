@@ -2,7 +2,7 @@
 # r6d (4 GPUs): in-step AlexNet N=4, alternating order on one box: ce (default) vs cet
 # (copy engines + TMA-fed owner fold) at 64/96 CTAs vs ceb (copy-engine reduce-scatter +
 # TMA owner + TMA all-gather) at 32/64 CTAs; N=4 sweep of ceb; GoogLeNet N=4 ce vs cet64.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6d
 mkdir -p $O

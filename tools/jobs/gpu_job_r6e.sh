@@ -2,7 +2,7 @@
 # r6e (4 GPUs): warp-specialised owner_tma (producer thread + consumer warps, full/done
 # mbarriers per stage): parity (1 GPU stepped, 4 GPUs concurrent), ncu of the stepped bulk
 # and cet owner kernels (vs r6a 253 us / r6c 26 us), sweeps, in-step N=4 ce vs bulk vs cet.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6e
 mkdir -p $O

@@ -2,7 +2,7 @@
 # r6h (4 GPUs): where the N=4 step's ~0.1 ms over compute goes: fwd+bwd alone (no optimizer)
 # at B=256/128/64, traced timelines (CSV per rank) for ce and bulk 48, exchange streams at
 # normal priority for the large layers (--low-priority-from 1M) vs the default high priority.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6h
 mkdir -p $O

@@ -2,7 +2,7 @@
 # r6i (4 GPUs): GoogLeNet step vs its compute (N=1 at B=32 = fwd+bwd + a 7 M-param update),
 # gate layer vs model at N=4; AlexNet NCCL comparison rows (DDP, bulk-synchronous NCCL) on
 # the current build at N=4 and N=2; AlexNet N=2 with the TMA bulk kernel at 48 CTAs.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6i
 mkdir -p $O

@@ -2,7 +2,7 @@
 # r6j (4 GPUs): GoogLeNet N=4 (9.82 ms/step vs 9.36 ms at N=1, B=32): the small layers'
 # exchange launches with capped grids (fewer SMs taken from the backward), at normal stream
 # priority, and without the L128 band.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6j
 mkdir -p $O

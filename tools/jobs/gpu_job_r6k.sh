@@ -2,7 +2,7 @@
 # r6k (4 GPUs): overlap_ctas — the small layers hidden behind the backward on capped grids,
 # layer 0 (the exposed one) on the full grid: parity (GoogLeNet plans, 1 GPU stepped) and
 # in-step GoogLeNet N=4 / AlexNet N=4 and N=2, alternating with the uncapped default.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6k
 mkdir -p $O

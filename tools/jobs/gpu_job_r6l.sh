@@ -3,7 +3,7 @@
 # then bench lines with the final defaults: AlexNet N=4 (x2) / N=2, GoogLeNet N=4 (model and
 # layer gates), configs[0] LeNet 2-rank and configs[1] cifar10_quick 4-rank with their
 # reference arms, AlexNet N=4 with --large cet.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6l
 mkdir -p $O

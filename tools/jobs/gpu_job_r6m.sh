@@ -1,7 +1,7 @@
 #!/bin/bash
 # r6m (4 GPUs): how many of the last-emitted layers should keep the full grid
 # (--overlap-exposed 1/2/3/5), GoogLeNet N=4 and AlexNet N=4, alternating.
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6m
 mkdir -p $O

@@ -1,7 +1,7 @@
 #!/bin/bash
 # r6n (4 GPUs): GoogLeNet N=4 --overlap-exposed sweep (r6m: 5 gave 9.31 ms vs 9.62 for 1 and
 # 9.66-9.68 for 2/3): 4, 5, 6, 8, 12 and repeats; AlexNet with 5 (= every conv layer full).
-cd "$(dirname "$0")/.." || exit 1
+cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
 R=r6n
 mkdir -p $O
