@@ -1,10 +1,10 @@
 #!/bin/bash
-# r6g (1 GPU): one-rank fused update with 4 K-element items (kN1Chunk): N=1 sweep, full -m gpu
+# r6o (1 GPU): final rehearsal of the round-2 build: N=1 update sweep, full -m gpu suite + smoke,
 # suite + smoke, N=1 bench x2, the bench's launch list (ncu gpu__time_duration) and an
 # ncu --set full capture of the fc6 update (traffic for roofline.traffic).
 cd "$(dirname "$0")/../.." || exit 1
 O=gpurun_out
-R=${R:-r6g}
+R=${R:-r6o}
 mkdir -p $O
 timeout 600 python tools/prof_update.py 16384:0 16384:296 > $O/${R}_prof_update.jsonl 2> $O/${R}_prof_update.err; echo "prof rc=$?"
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/${R}_pytest_gpu_1gpu.log 2>&1; echo "suite rc=$?"
