@@ -80,6 +80,23 @@ def choose_variant(elems: int, world: int, tree_below: int = 0, ce_from: int = 1
     return "twoshot"
 
 
+def layer_ctas(elems, world: int, *, large_from: int = 1 << 20, large_ctas: int = 0, overlap_ctas: int = 0,
+               overlap_exposed: int = 1) -> list[int]:
+    """Per-layer CTA caps (0 = the library default) of an exchange plan: layers of
+    >= `large_from` elements get `large_ctas`; with `overlap_ctas` (N > 1) every smaller layer
+    but the first `overlap_exposed` ones (the last gradients backward emits, whose exchange
+    nothing hides) runs on at most `overlap_ctas` CTAs (DeviceExchange, variant="auto")."""
+    caps = []
+    for l, n in enumerate(elems):
+        if n >= large_from:
+            caps.append(int(large_ctas))
+        elif overlap_ctas > 0 and world > 1 and l >= max(1, overlap_exposed):
+            caps.append(int(overlap_ctas))
+        else:
+            caps.append(0)
+    return caps
+
+
 class DeviceExchange:
     def __init__(self, transport, layer_elems, *, mode: str = "fast32", variant="twoshot",
                  chunk_elems: int = 16384, lr: float = 0.01, scale: float | None = None,
@@ -142,9 +159,9 @@ class DeviceExchange:
         big = [n >= large_from for n in self.layer_elems]
         chunks = list(layer_chunk_elems) if layer_chunk_elems is not None else \
             [int(large_chunk_elems) if b else 0 for b in big]
-        ctas = list(layer_max_ctas) if layer_max_ctas is not None else [int(large_ctas) if b else 0 for b in big]
-        if layer_max_ctas is None and auto and overlap_ctas > 0 and self.world > 1 and not max_ctas:
-            ctas = [c if (b or l < max(1, overlap_exposed)) else int(overlap_ctas) for l, (c, b) in enumerate(zip(ctas, big))]
+        ctas = list(layer_max_ctas) if layer_max_ctas is not None else \
+            layer_ctas(self.layer_elems, self.world, large_from=large_from, large_ctas=large_ctas,
+                       overlap_ctas=overlap_ctas if (auto and not max_ctas) else 0, overlap_exposed=overlap_exposed)
         if len(chunks) != L or len(ctas) != L:
             raise ConfigError("layer_chunk_elems / layer_max_ctas need one entry per layer")
         self._chunks_req = [int(c) for c in chunks]

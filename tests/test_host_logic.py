@@ -158,3 +158,31 @@ def test_variant_policy():
     assert choose_variant(37_752_832, 4, large="cep") == "twoshot_cep"
     assert choose_variant(37_752_832, 1, ll_below=ll) == "twoshot"        # N=1: the fused update
     assert choose_variant(1000, 8, tree_below=4096, ll_below=ll) == "tree"
+
+
+ALEXNET = [34944, 307456, 885120, 663936, 442624, 37752832, 16781312, 4097000]
+
+
+def test_overlap_grid_caps_policy():
+    """bench.py's default plan: every small layer but layer 0 (the last gradient backward
+    emits) on a 16-CTA grid, large layers on their own cap, nothing capped at one rank."""
+    from paper_1706_00095_b200.exchange import layer_ctas
+
+    assert layer_ctas(ALEXNET, 4, overlap_ctas=16) == [0, 16, 16, 16, 16, 0, 0, 0]
+    assert layer_ctas(ALEXNET, 4, overlap_ctas=16, large_ctas=48) == [0, 16, 16, 16, 16, 48, 48, 48]
+    assert layer_ctas(ALEXNET, 4, overlap_ctas=16, overlap_exposed=3) == [0, 0, 0, 16, 16, 0, 0, 0]
+    assert layer_ctas(ALEXNET, 1, overlap_ctas=16) == [0] * 8
+    assert layer_ctas(ALEXNET, 4, overlap_ctas=0) == [0] * 8
+
+
+def test_auto_variant_policy_alexnet():
+    """The layer-size policy bench.py runs at N=4 (LL one-shot <= 64 K elements, the
+    128-byte-line two-shot in (64 K, 1 M), copy engines >= 1 M) and its large-layer options."""
+    from paper_1706_00095_b200.exchange import L128_BAND, VARIANT_ALIASES, choose_variant
+
+    plan = [choose_variant(n, 4, ll_below=1 << 16, l128_range=L128_BAND) for n in ALEXNET]
+    assert plan == ["oneshot_ll"] + ["twoshot_l128"] * 4 + ["twoshot_ce"] * 3
+    for large, want in (("bulk", "twoshot_bulk"), ("cet", "twoshot_cet"), ("ceb", "twoshot_ceb"), ("sm", "twoshot")):
+        assert choose_variant(ALEXNET[5], 4, large=large) == want
+    assert VARIANT_ALIASES["twoshot_cet"] == ("twoshot_ce", "ce_tma_owner")
+    assert choose_variant(ALEXNET[5], 1) == "twoshot"  # one rank: the fused update alone
