@@ -67,6 +67,7 @@ def parse():
     p.add_argument("--overlap-ctas", type=int, default=16,
                    help="CTA cap of the small layers whose exchange overlaps the backward (all but layer 0); "
                         "0 = off (profiles/r6k: GoogLeNet N=4 +1.8 %%, AlexNet N=4 +0.9 %%)")
+    p.add_argument("--ce-parts", type=int, default=0, help="copy-engine owner pipelining depth (0 = library default 4)")
     p.add_argument("--overlap-exposed", type=int, default=1,
                    help="how many of the first layers (emitted last by backward) keep the full grid")
     p.add_argument("--l128", default="%d:%d" % L128_BAND,
@@ -290,7 +291,8 @@ def workload_config(world, args):
                                                                "chunk_elems": args.large_chunk_elems},
             "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager",
             "exchange_flags": args.xflags or None, "l128_range": args.l128 or None,
-            "overlap_ctas": args.overlap_ctas, "overlap_exposed": args.overlap_exposed}
+            "overlap_ctas": args.overlap_ctas, "overlap_exposed": args.overlap_exposed,
+            "ce_parts": args.ce_parts or None}
 
 
 # ------------------------------------------------------------------ model
@@ -429,7 +431,7 @@ def pgx_arm(args):
                           low_priority_from=args.low_priority_from or None, large=args.large,
                           large_ctas=args.large_ctas, large_chunk_elems=args.large_chunk_elems,
                           flags=xflags_of(args), l128_range=l128_of(args), overlap_ctas=args.overlap_ctas,
-                          overlap_exposed=args.overlap_exposed,
+                          overlap_exposed=args.overlap_exposed, ce_parts=args.ce_parts,
                           **wl["hyper"])
     gate = args.gate if args.gate != "auto" else ("model" if len(sizes) > 16 else "layer")
     bind = ModuleBinding(xchg, model.layers(), gate=gate)
