@@ -623,6 +623,12 @@ def pgx_arm(args):
     timeline = trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world)
     timeline.update(pipelined_vs_barrier(bind, step, dev_x, dev_y, world))
 
+    # ---- the same forward + backward with the exchange switched off (hooks drop the
+    # gradients, gates pass): what the step would cost with a free exchange ----
+    alone = fwd_bwd_alone(args, bind, model, dev_x, dev_y, dev, world, barrier)
+    alone["exchange_overhead_ms"] = ms / args.steps - alone["ms_per_step"]
+    alone["step_over_fwd_bwd"] = (ms / args.steps) / alone["ms_per_step"]
+
     # ---- per-layer exchange in isolation (same launch, no concurrent backward, host enqueue
     # latency hidden behind a busy kernel so the events bracket device time): every rank,
     # device flag barrier before each, launch -> own part done -> gate on all arrivals.  The
@@ -778,7 +784,7 @@ def pgx_arm(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": wl["scaling"],
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
-            "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None, "timeline": timeline,
+            "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None, "timeline": timeline, "fwd_bwd_alone": alone,
             "exchange_by_layer": by_layer or None, "exchange_by_layer_sm_twoshot": by_layer_sm or None}
     # ---- exchange only: the whole model's exchange per iteration, GPU (device time, every layer
     # back to back, no backward) vs the CPU reference at the same world size (rank 0 only) ----
@@ -813,6 +819,55 @@ def pgx_arm(args):
     tr.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def fwd_bwd_alone(args, bind, model, dev_x, dev_y, dev, world, barrier, reps=10):
+    """Forward + backward of the benched model alone (ModuleBinding.disabled: no exchange
+    launch, no gate, gradients dropped), replayed from its own CUDA graph like the step,
+    device time per step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    def body():
+        xin = dev_x.to(torch.bfloat16, memory_format=torch.channels_last).sub_(128.0).mul_(1.0 / 64.0)
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            out = model(xin)
+        model.loss(out, dev_y).backward()
+
+    bind.disabled = True
+    try:
+        for _ in range(3):
+            body()
+        torch.cuda.synchronize()
+        run = body
+        if not args.no_graph:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(device=dev)
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+                body()
+            torch.cuda.current_stream().wait_stream(s)
+            run = g.replay
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / reps
+        if world > 1:
+            tt = torch.tensor([t])
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+    finally:
+        bind.disabled = False
+    return {"ms_per_step": t, "reps": reps,
+            "measured": "same model and inputs, exchange hooks and gates disabled, "
+                        + ("CUDA-graph replays" if not args.no_graph else "eager steps") + ", max over ranks"}
 
 
 def trace_timeline(args, bind, model, step, dev_x, dev_y, rank, world, steps=3):

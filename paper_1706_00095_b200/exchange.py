@@ -414,9 +414,13 @@ class ModuleBinding:
         self.trace = None                # list -> record (iteration, layer, ready_event, done_event)
         self.events: dict = {}
         self.deferred = None             # list -> phase-separated schedule: hooks queue, flush() launches
+        self.disabled = False            # measurement only: hooks drop the gradients, gates pass (no exchange)
 
     def _make_hook(self, l):
         def hook(_p):
+            if self.disabled:
+                _p.grad = None
+                return
             self._pending[l] += 1
             params = self.layers[l][1]
             if self._pending[l] < len(params):
@@ -464,6 +468,8 @@ class ModuleBinding:
 
     def _make_gate(self, l):
         def pre_hook(_mod, _inp):
+            if self.disabled:
+                return
             if self.gate_mode == "model":
                 if self._gated_step == self.k:
                     return
