@@ -77,6 +77,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--timeline", default="")
+    p.add_argument("--trace-graph", action="store_true",
+                   help="diagnostic: bracket every layer's exchange with events inside the step graph and "
+                        "report them (graph_trace) relative to the step start / backward end")
     p.add_argument("--per-gpu-batch", type=int, default=0,
                    help="diagnostic only: override 256/N (the line is then not the headline config)")
     return p.parse_args()
@@ -494,7 +497,10 @@ def pgx_arm(args):
     # ---- capture one training step as a CUDA graph (epochs from the device counter) ----
     graph = None
     bind.timed_layers = {L_DOM}  # bracket the dominant layer's exchange with (external) events
+    if args.trace_graph:
+        bind.timed_layers = set(range(len(sizes)))
     bind.events.clear()
+    gmarks = None
     if not args.no_graph:
         k_before_capture = bind.k
         xchg.set_device_iteration(True, bind.k - 1)
@@ -505,8 +511,15 @@ def pgx_arm(args):
         with torch.cuda.stream(cap):
             with torch.cuda.graph(graph, stream=cap):
                 bind.begin_step()
+                if args.trace_graph:
+                    gmarks = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)]
+                    gmarks[0].record()
                 static_loss = step(dev_x, dev_y)
+                if gmarks:
+                    gmarks[1].record()  # the compute stream is past the backward
                 bind.drain()  # joins every exchange stream back into the capture
+                if gmarks:
+                    gmarks[2].record()
         per_step_launches = xchg.launch_count() - c0
         torch.cuda.current_stream().wait_stream(cap)
         torch.cuda.synchronize()
@@ -602,6 +615,7 @@ def pgx_arm(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * world, "ms_per_step": ms_e2e / args.steps,
                "final_loss": float(loss_host[(args.steps - 1) % loss_host.numel()])}
 
+    graph_trace = None
     # ---- dominant-layer exchange time inside steps: the events captured in the graph (or
     # recorded by every eager step) bracket that layer's exchange on its streams ----
     durs = []
@@ -611,6 +625,14 @@ def pgx_arm(args):
             torch.cuda.synchronize()
             a, b_ = bind.events[L_DOM][0]
             durs.append(a.elapsed_time(b_))
+        if gmarks:  # the last replay's per-layer exchange spans on the device clock
+            z = gmarks[0]
+            graph_trace = {"backward_end_ms": z.elapsed_time(gmarks[1]), "step_end_ms": z.elapsed_time(gmarks[2]),
+                           "layers": [[l, round(z.elapsed_time(bind.events[l][0][0]), 4),
+                                       round(z.elapsed_time(bind.events[l][0][1]), 4)]
+                                      for l in sorted(bind.events)],
+                           "note": "[layer, exchange launch (gradient ready), this rank's part done] ms from the "
+                                   "start of the captured step; diagnostic run (--trace-graph)"}
         bind.wait_current()
         torch.cuda.synchronize()
         bind.k = k_before_capture + replays[0]  # continue the epoch sequence eagerly after the replays
@@ -785,6 +807,7 @@ def pgx_arm(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (uint8 images, random labels; random-init "
             "weights)", "config": workload_config(world, args), "roofline": roof, "clocks": clk,
             "gpu_launches": launches, "e2e": e2e, "cuda_graph": graph is not None, "timeline": timeline, "fwd_bwd_alone": alone,
+            "graph_trace": graph_trace,
             "exchange_by_layer": by_layer or None, "exchange_by_layer_sm_twoshot": by_layer_sm or None}
     # ---- exchange only: the whole model's exchange per iteration, GPU (device time, every layer
     # back to back, no backward) vs the CPU reference at the same world size (rank 0 only) ----

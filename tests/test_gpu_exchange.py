@@ -169,6 +169,42 @@ def test_module_binding_single_gpu_matches_sgd_rule(cuda):
     world.close()
 
 
+def test_module_binding_disabled_launches_nothing(cuda):
+    """bench.py's fwd_bwd_alone: with the binding disabled a backward launches no exchange,
+    gates nothing, leaves the weights untouched and drops the gradients; re-enabled, the
+    next step exchanges as usual."""
+    from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
+    from paper_1706_00095_b200.transport import LocalWorld
+
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(16, 8), torch.nn.ReLU(), torch.nn.Linear(8, 4)).cuda()
+    layers = [(m, [m.weight, m.bias]) for m in (net[0], net[2])]
+    elems = [sum(p.numel() for p in ps) for _, ps in layers]
+    world = LocalWorld(1, inline=False)
+    x = DeviceExchange(world.transport(0), elems, mode="fast32", lr=0.1, momentum=0.9)
+    x.connect()
+    bind = ModuleBinding(x, layers)
+    data = torch.randn(5, 16, device="cuda")
+    before = x.model.clone()
+    n0, l0 = x.launch_count(), bind.gpu_launches
+    bind.disabled = True
+    net(data).square().mean().backward()
+    torch.cuda.synchronize()
+    assert x.launch_count() == n0 and bind.gpu_launches == l0
+    assert torch.equal(x.model, before)
+    assert all(p.grad is None for _, ps in layers for p in ps)
+    bind.disabled = False
+    net(data).square().mean().backward()
+    bind.step_done()
+    bind.drain()
+    torch.cuda.synchronize()
+    assert bind.gpu_launches > l0 and not torch.equal(x.model, before)
+    assert x.tr.device_status() == 0
+    bind.remove()
+    x.close()
+    world.close()
+
+
 class _FixedGrad(torch.nn.Module):
     """loss = sum(w * c) + sum(b * d): its gradient is exactly (c, d) every step (no GEMM
     rounding), so graph replays and eager steps must both equal the oracle bit for bit."""
