@@ -231,9 +231,12 @@ enum pgx_xchg_flag {
   PGX_XF_BULK_CE_RS = 128,         /* TWOSHOT_BULK: reduce-scatter by the copy engines in
                                       part-major copies (per-part chunk signals); the kernel
                                       runs the owner slabs only (fold + update + TMA gather) */
-  PGX_XF_CE_TMA_OWNER = 256        /* TWOSHOT_CE: owner fold fed by TMA bulk loads on a capped
+  PGX_XF_CE_TMA_OWNER = 256,       /* TWOSHOT_CE: owner fold fed by TMA bulk loads on a capped
                                       grid (layer_max_ctas, default 32) instead of the LSU
                                       fold on every SM                                      */
+  PGX_XF_LEAN_CAPPED = 512         /* ONESHOT_LL / TWOSHOT_L128 layers with a layer_max_ctas
+                                      cap launch 128-thread CTAs (fewer SM slots held while
+                                      they poll for their peers, next to the backward)      */
 };
 
 typedef struct pgx_xchg_config {

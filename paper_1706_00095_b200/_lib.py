@@ -35,6 +35,7 @@ XF_CE_RS_PARTS, XF_TMA, XF_ONESHOT_SMALL_CHUNKS, XF_AUTO_CHUNK_TREE, XF_NO_AUTO_
 XF_BULK_LEAN = 64
 XF_BULK_CE_RS = 128
 XF_CE_TMA_OWNER = 256
+XF_LEAN_CAPPED = 512
 PHASE_PUSH, PHASE_OWNER, PHASE_DOWN, PHASE_ALL = 1, 2, 4, 7
 
 vp = C.c_void_p

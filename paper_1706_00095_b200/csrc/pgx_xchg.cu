@@ -1885,6 +1885,7 @@ __global__ void __launch_bounds__(kThreads) k_owner_local(XArgs a) {
 
 constexpr int kCepCtas = 48;  // TWOSHOT_CEP owner grid default
 constexpr int kCeTmaCtas = 32;  // TWOSHOT_CE + PGX_XF_CE_TMA_OWNER owner grid default
+constexpr int kLeanThreads = 128;  // PGX_XF_LEAN_CAPPED: threads per CTA of capped LL / L128 layers
 constexpr uint64_t kAutoChunkMax = 65536;  // elements
 constexpr uint64_t kN1Chunk = 4096;        // elements per item of a one-rank (update-only) launch
 
@@ -1955,6 +1956,7 @@ struct LayerPlan {
   uint32_t Co = 0;       // TWOSHOT_L128: owner items
   int grid = 0, down_grid = 0;
   uint64_t nvlink_bytes = 0, hbm_bytes = 0;
+  bool lean = false;     // LL / L128 layer with a CTA cap under PGX_XF_LEAN_CAPPED: 128-thread CTAs
 };
 
 }  // namespace
@@ -2229,22 +2231,22 @@ int twoshot_l128_grid(int want, int dev) {
   return std::max(1, std::min(want, cap[dev]));
 }
 
-void launch_twoshot_l128(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
+void launch_twoshot_l128(int N, int want, int dev, cudaStream_t s, const XArgs& a, int threads = kThreads) {
   switch (N) {
 #define PGX_CASE(n)                                                                \
   case n:                                                                          \
-    k_twoshot_l128<n><<<twoshot_l128_grid<n>(want, dev), kThreads, 0, s>>>(a);     \
+    k_twoshot_l128<n><<<twoshot_l128_grid<n>(want, dev), threads, 0, s>>>(a);     \
     break;
     PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
 #undef PGX_CASE
   }
 }
 
-void launch_oneshot_ll(int N, int want, int dev, cudaStream_t s, const XArgs& a) {
+void launch_oneshot_ll(int N, int want, int dev, cudaStream_t s, const XArgs& a, int threads = kThreads) {
   switch (N) {
 #define PGX_CASE(n)                                                            \
   case n:                                                                      \
-    k_oneshot_ll<n><<<oneshot_ll_grid<n>(want, dev), kThreads, 0, s>>>(a);   \
+    k_oneshot_ll<n><<<oneshot_ll_grid<n>(want, dev), threads, 0, s>>>(a);   \
     break;
     PGX_CASE(1) PGX_CASE(2) PGX_CASE(3) PGX_CASE(4) PGX_CASE(5) PGX_CASE(6) PGX_CASE(7) PGX_CASE(8)
 #undef PGX_CASE
@@ -2900,6 +2902,8 @@ int pgx_xchg_create(pgx_world* w, const pgx_xchg_config* cfg, pgx_xchg** out) {
     const bool lcapped = cfg->layer_max_ctas && cfg->layer_max_ctas[l] > 0;
     int cap = lcapped ? cfg->layer_max_ctas[l] : cap_all;
     bool capped = lcapped || cfg->max_ctas > 0;
+    P.lean = (cfg->flags & PGX_XF_LEAN_CAPPED) && lcapped &&
+             (P.variant == PGX_VARIANT_ONESHOT_LL || P.variant == PGX_VARIANT_TWOSHOT_L128);
     if (P.variant == PGX_VARIANT_TWOSHOT_CEP && !capped) {  // 48 CTAs saturate NVLink (profiles/r3h)
       cap = std::min(cap, kCepCtas);
       capped = true;
@@ -3239,7 +3243,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
       ++x->launches;
       const int want = (int)std::min<uint32_t>(a.item_end - a.item_begin, (uint32_t)P.grid);
       if (P.variant == PGX_VARIANT_ONESHOT_LL)
-        launch_oneshot_ll(x->world, want, x->dev, s, a);
+        launch_oneshot_ll(x->world, want, x->dev, s, a, P.lean ? kLeanThreads : kThreads);
       else
         launch_oneshot_l128(x->world, want, x->dev, s, a);
     }
@@ -3258,7 +3262,7 @@ int pgx_xchg_layer(pgx_xchg* x, int l, uint32_t iteration, const void* const* pi
     if (a.item_end > a.item_begin) {
       ++x->launches;
       const int want = (int)std::min<uint32_t>(a.item_end - a.item_begin, (uint32_t)P.grid);
-      launch_twoshot_l128(x->world, want, x->dev, s, a);
+      launch_twoshot_l128(x->world, want, x->dev, s, a, P.lean ? kLeanThreads : kThreads);
     }
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = xrecord(x->done[l], s);

@@ -36,7 +36,7 @@ VARIANT_ALIASES = {"twoshot_ceb": ("twoshot_bulk", "bulk_ce_rs"),  # Python name
 FLAGS = {"ce_rs_parts": _lib.XF_CE_RS_PARTS, "tma": _lib.XF_TMA, "oneshot_small_chunks": _lib.XF_ONESHOT_SMALL_CHUNKS,
          "auto_chunk_tree": _lib.XF_AUTO_CHUNK_TREE, "no_auto_chunk_nvls": _lib.XF_NO_AUTO_CHUNK_NVLS,
          "allow_l128": _lib.XF_ALLOW_L128, "bulk_lean": _lib.XF_BULK_LEAN, "bulk_ce_rs": _lib.XF_BULK_CE_RS,
-         "ce_tma_owner": _lib.XF_CE_TMA_OWNER}
+         "ce_tma_owner": _lib.XF_CE_TMA_OWNER, "lean_capped": _lib.XF_LEAN_CAPPED}
 MODES = {"ref64": _lib.MODE_REF64, "ref32": _lib.MODE_REF32, "fast32": _lib.MODE_FAST32, "sum32": _lib.MODE_SUM32}
 
 

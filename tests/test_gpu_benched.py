@@ -53,13 +53,14 @@ def _expected_variants(sizes, N, mode, large="ce"):
     return [choose_variant(n, N, 0, ce_from=1 << 20, large=large, ll_below=ll, l128_range=band) for n in sizes]
 
 
-def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER, large="ce", overlap_ctas=16):
+def _run(N, sizes, mode, iters, gate, fast_hyper=HYPER, large="ce", overlap_ctas=16, flags=()):
     from paper_1706_00095_b200.exchange import L128_BAND
 
     hyper = fast_hyper if mode == "fast32" else dict(lr=0.05)
     # bench.py's defaults: --l128 = L128_BAND (with the allow_l128 opt-in), large layers "ce",
     # --overlap-ctas 16
-    world, trs, xs = build(N, sizes, mode, "auto", chunk_elems=16384, flags=("allow_l128",), l128_range=L128_BAND,
+    world, trs, xs = build(N, sizes, mode, "auto", chunk_elems=16384, flags=("allow_l128",) + tuple(flags),
+                           l128_range=L128_BAND,
                            large=large, overlap_ctas=overlap_ctas, **hyper)
     if overlap_ctas:  # every small layer but layer 0 runs on the capped grid
         caps = [xs[0].layer_plan(l)[1] for l in range(len(sizes))]
@@ -127,12 +128,13 @@ def test_alexnet_plan_has_multipart_owners(cuda):
 
 
 @pytest.mark.parametrize("N", [4, 8])
-@pytest.mark.parametrize("overlap_ctas", [0, 16])
-def test_googlenet_auto_plan_model_gate_matches_oracle(cuda, N, overlap_ctas):
+@pytest.mark.parametrize("overlap_ctas,lean", [(0, False), (16, False), (16, True)])
+def test_googlenet_auto_plan_model_gate_matches_oracle(cuda, N, overlap_ctas, lean):
     """GoogLeNet's 64 layers (12 KB .. 8 MB) with the whole-model gate bench.py uses for
     nets of > 16 layers: LL / one-shot / two-shot / copy-engine layers in one step; also
     with the hidden small layers on 16-CTA grids (bench.py --overlap-ctas)."""
-    _run(N, _googlenet_sizes(), "fast32", iters=2, gate="model", overlap_ctas=overlap_ctas)
+    _run(N, _googlenet_sizes(), "fast32", iters=2, gate="model", overlap_ctas=overlap_ctas,
+         flags=("lean_capped",) if lean else ())
 
 
 @pytest.mark.parametrize("workload,N", [("lenet", 2), ("cifar10_quick", 4)])
