@@ -77,6 +77,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--timeline", default="")
+    p.add_argument("--graph-prio", action="store_true",
+                   help="diagnostic: instantiate the step graph with the capture streams' priorities on its "
+                        "nodes (pgx_graph_instantiate_prio); dropout masks then repeat across replays")
     p.add_argument("--trace-graph", action="store_true",
                    help="diagnostic: bracket every layer's exchange with events inside the step graph and "
                         "report them (graph_trace) relative to the step start / backward end")
@@ -295,6 +298,7 @@ def workload_config(world, args):
             "gate": args.gate, "step": "CUDA graph replay" if not args.no_graph else "eager",
             "exchange_flags": args.xflags or None, "l128_range": args.l128 or None,
             "overlap_ctas": args.overlap_ctas, "overlap_exposed": args.overlap_exposed,
+            "graph_prio": args.graph_prio or None,
             "ce_parts": args.ce_parts or None}
 
 
@@ -504,7 +508,7 @@ def pgx_arm(args):
     if not args.no_graph:
         k_before_capture = bind.k
         xchg.set_device_iteration(True, bind.k - 1)
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=args.graph_prio)
         cap = torch.cuda.Stream(device=dev)
         cap.wait_stream(torch.cuda.current_stream())
         c0 = xchg.launch_count()
@@ -524,12 +528,23 @@ def pgx_arm(args):
         torch.cuda.current_stream().wait_stream(cap)
         torch.cuda.synchronize()
         replays = [0]
+        prio_exec = None
+        if args.graph_prio:
+            import ctypes
+
+            from paper_1706_00095_b200 import _lib
+            ex = ctypes.c_void_p()
+            _lib.call("pgx_graph_instantiate_prio", ctypes.c_void_p(graph.raw_cuda_graph()), ctypes.byref(ex))
+            prio_exec = ex
 
         def run_step(xb=None, yb=None):
             if xb is not None:
                 dev_x.copy_(xb, non_blocking=True)
                 dev_y.copy_(yb, non_blocking=True)
-            graph.replay()
+            if prio_exec is not None:
+                _lib.call("pgx_graph_launch", prio_exec, ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
+            else:
+                graph.replay()
             replays[0] += 1
             return static_loss
 

@@ -333,6 +333,14 @@ int pgx_xchg_layer_parts(pgx_xchg* x, int layer, int* parts_out);
  * NULL turns it off (the default: one predicated-off branch per item). */
 int pgx_xchg_set_trace(pgx_xchg* x, void* device_buffer);
 
+/* Step graphs (no reference counterpart: the captured training step of bench.py).
+ * Instantiate a captured cudaGraph_t with the capture streams' priorities kept on its
+ * kernel nodes (cudaGraphInstantiateFlagUseNodePriority: the exchange stream's high
+ * priority survives into the replays), launch it on `stream`, destroy the executable. */
+int pgx_graph_instantiate_prio(void* graph, void** exec_out);
+int pgx_graph_launch(void* exec, void* stream);
+int pgx_graph_exec_destroy(void* exec);
+
 #ifdef __cplusplus
 }
 #endif

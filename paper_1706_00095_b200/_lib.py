@@ -116,6 +116,9 @@ SIGNATURES = {
     "pgx_xchg_layer_plan": [vp, i32, P(u64), P(i32)],
     "pgx_xchg_layer_parts": [vp, i32, P(i32)],
     "pgx_xchg_set_trace": [vp, vp],
+    "pgx_graph_instantiate_prio": [vp, P(vp)],
+    "pgx_graph_launch": [vp, vp],
+    "pgx_graph_exec_destroy": [vp],
     "pgx_xchg_launch_count": [vp, P(u64)],
     "pgx_xchg_stream": [vp, i32, P(vp)],
     "pgx_xchg_set_streams": [vp, P(vp), i32],

@@ -3516,6 +3516,27 @@ int pgx_xchg_set_trace(pgx_xchg* x, void* device_buffer) {
   return PGX_OK;
 }
 
+int pgx_graph_instantiate_prio(void* graph, void** exec_out) {
+  if (!graph || !exec_out) return fail(PGX_E_CONFIG, "graph and exec_out must be non-null");
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaGraphInstantiateWithFlags(&ex, static_cast<cudaGraph_t>(graph), cudaGraphInstantiateFlagUseNodePriority);
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "cudaGraphInstantiateWithFlags: %s", cudaGetErrorString(e));
+  *exec_out = ex;
+  return PGX_OK;
+}
+
+int pgx_graph_launch(void* exec, void* stream) {
+  cudaError_t e = cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
+int pgx_graph_exec_destroy(void* exec) {
+  cudaError_t e = cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
+  if (e != cudaSuccess) return fail(PGX_E_CUDA, "cudaGraphExecDestroy: %s", cudaGetErrorString(e));
+  return PGX_OK;
+}
+
 int pgx_xchg_layer_plan(pgx_xchg* x, int l, uint64_t* chunk_elems, int* ctas) {
   if (l < 0 || l >= (int)x->L.size()) return fail(PGX_E_RANGE, "layer %d outside 0..%d", l, (int)x->L.size() - 1);
   if (chunk_elems) *chunk_elems = x->L[l].CH;
