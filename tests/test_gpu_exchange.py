@@ -455,3 +455,58 @@ def test_misaligned_gradient_views_match_oracle(cuda, variant):
     for x in xs:
         x.close()
     world.close()
+
+
+def test_graph_instantiated_with_node_priorities_replays_the_exchange(cuda):
+    """pgx_graph_instantiate_prio / pgx_graph_launch (bench.py --graph-prio): a captured
+    training step launched through the library's executable applies exactly the oracle
+    update, replay after replay, like torch's own replay."""
+    import ctypes
+
+    from paper_1706_00095_b200 import _lib
+    from paper_1706_00095_b200.exchange import DeviceExchange, ModuleBinding
+    from paper_1706_00095_b200.transport import LocalWorld
+
+    m = _FixedGrad(40000, 6)
+    layers = [(m, [m.weight, m.bias])]
+    world = LocalWorld(1, inline=False)
+    tr = world.transport(0)
+    x = DeviceExchange(tr, [40007], mode="fast32", lr=0.05, momentum=0.9, weight_decay=1e-3)
+    x.connect()
+    w = torch.cat([m.weight.detach(), m.bias.detach()]).cpu().numpy()
+    g = torch.cat([m.c, m.d]).cpu().numpy()
+    bind = ModuleBinding(x, layers)
+    v = np.zeros_like(w)
+
+    def step():
+        m().backward()
+        bind.step_done()
+
+    step()
+    bind.drain()
+    torch.cuda.synchronize()
+    x.set_device_iteration(True, bind.k - 1)
+    graph = torch.cuda.CUDAGraph(keep_graph=True)
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap), torch.cuda.graph(graph, stream=cap):
+        bind.begin_step()
+        step()
+        bind.drain()
+    torch.cuda.current_stream().wait_stream(cap)
+    torch.cuda.synchronize()
+    ex = ctypes.c_void_p()
+    _lib.call("pgx_graph_instantiate_prio", ctypes.c_void_p(graph.raw_cuda_graph()), ctypes.byref(ex))
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        _lib.call("pgx_graph_launch", ex, ctypes.c_void_p(s.cuda_stream))
+    bind.wait_current()
+    torch.cuda.synchronize()
+    _lib.call("pgx_graph_exec_destroy", ex)
+    for _ in range(1 + 3):  # the eager step before the capture + 3 launches (capturing runs nothing)
+        w, v = O.fast32_update(w, v, g, 1.0, 0.05, 0.9, 1e-3)
+    assert tr.device_status() == 0
+    assert x.layer_views[0].cpu().numpy().tobytes() == w.tobytes()
+    bind.remove()
+    x.close()
+    world.close()
