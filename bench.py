@@ -473,25 +473,6 @@ def pgx_arm(args):
         if world > 1:
             dist.barrier()
 
-    def timed(fn, k):
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(k):
-            fn(i)
-        bind.drain()  # the last iteration's weights are installed everywhere
-        e1.record()
-        torch.cuda.synchronize()
-        barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms])
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
-
     for _ in range(args.warmup):
         step(dev_x, dev_y)
     bind.drain()
